@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-vector engine (BASELINE.json metric: gates/s and
+circuit time, % of the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config layered28|qft30|layered33|layered-N|qft-N] [--precision single|double]
+
+One *step* = one full circuit: |0...0> preparation plus every planned pass of
+the fused circuit, inputs (the state) resident in HBM.  The default N=1
+workload is BASELINE config 2: the seeded 28-qubit layered circuit (973 gates,
+fused to 189 at width 2) in complex64.  ``value`` counts ORIGINAL (unfused)
+gates per second.  For N>1 the state is sharded over the ranks (top log2 N
+qubits global) -- weak scaling: n = 28 + log2 N.
+
+``--impl reference`` times the reference's NumPy algorithm (the oracle port in
+oracle/, single-threaded like ref engines.py:190-203) on a bounded sample of the
+same workload: each step applies the next fused gate of the circuit at full n.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# sizeof(svb::PassArgs<C>) (csrc/svb_types.h): header 64 B + 48 ops x 80 B + 24 KiB pool
+PASS_ARGS_BYTES = 64 + 48 * 80 + 24576
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--precision", default=None, choices=[None, "single", "double"])
+    ap.add_argument("--fuse-width", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cost-budget", type=float, default=0.0)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--min-low-bits", type=int, default=0)
+    return ap.parse_args()
+
+
+def workload(args, world: int):
+    """(name, circuit, precision) for the configuration."""
+    from paper_2604_03816_b200 import generators as gen
+    from paper_2604_03816_b200.precision import select_precision
+
+    extra = int(round(math.log2(world))) if world > 1 else 0
+    cfg = args.config or "layered28"
+    if cfg == "layered28":
+        n, kind, prec = 28 + extra, "layered", "single"
+    elif cfg == "qft30":
+        n, kind, prec = 30 + extra, "qft", "double"
+    elif cfg == "layered33":
+        n, kind, prec = 33 + extra, "layered", "double"
+    elif cfg.startswith("layered-"):
+        n, kind, prec = int(cfg.split("-")[1]), "layered", "single"
+    elif cfg.startswith("qft-"):
+        n, kind, prec = int(cfg.split("-")[1]), "qft", "double"
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    if args.precision:
+        prec = args.precision
+    circuit = gen.layered_circuit(n) if kind == "layered" else gen.qft_circuit(n)
+    return cfg, kind, n, circuit, prec
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(circuit_fused, g0: int, n: int, prec: str, budget_s: float = 20.0) -> dict:
+    """Oracle (numpy restatement of ref engines.py kernels, 1 thread) on a
+    bounded sample: consecutive fused gates at full n until ``budget_s``."""
+    from oracle import sv_oracle as orc
+    t0 = time.perf_counter()
+    amps = orc.init_state(n, prec)
+    t_init = time.perf_counter() - t0
+    done = 0
+    t0 = time.perf_counter()
+    while done < len(circuit_fused.gates):
+        orc.apply_gate(amps, n, circuit_fused.gates[done])
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    per_fused = g0 / len(circuit_fused.gates)
+    return {"value": done * per_fused / dt, "unit": "gates/s", "cores": 1, "kind": "port",
+            "sample": f"first {done} of {len(circuit_fused.gates)} fused gates at n={n} {prec} "
+                      f"({dt:.1f} s, +{t_init:.1f} s init); gates/s counts original gates "
+                      f"({per_fused:.3f} per fused gate); host cpu_count={os.cpu_count()}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import sv_oracle as orc
+    from paper_2604_03816_b200.fusion import fuse
+    cfg, kind, n, circuit, prec = workload(args, world)
+    fused, _ = fuse(circuit, args.fuse_width)
+    g0, gf = len(circuit.gates), len(fused.gates)
+    amps = orc.init_state(n, prec)
+    times = []
+    for step in range(args.warmup + args.steps):
+        op = fused.gates[step % gf]
+        t0 = time.perf_counter()
+        orc.apply_gate(amps, n, op)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    per_fused = g0 / gf
+    total = sum(times)
+    value = len(times) * per_fused / total
+    line = {
+        "impl": "reference", "metric": "gates/s", "value": value, "unit": "gates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c64" if prec == "single" else "c128",
+        "data": "synthetic seeded circuit",
+        "config": {"workload": f"{cfg}: {kind}-{n} {prec}, fused {g0}->{gf} (width {args.fuse_width})",
+                   "n_qubits": n, "g_original": g0, "g_fused": gf},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port",
+                         "sample": f"one fused gate per step at full n={n} (oracle port of "
+                                   "ref engines.py:62-105, numpy single-threaded); circuit time "
+                                   f"extrapolates to {total / len(times) * gf:.1f} s"},
+        "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_03816_b200 import B200Engine, plan_options
+    from paper_2604_03816_b200.b200 import prec_code
+    from paper_2604_03816_b200.fusion import fuse
+    from paper_2604_03816_b200.precision import select_precision
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg, kind, n, circuit, prec = workload(args, world)
+    fused, rep = fuse(circuit, args.fuse_width)
+    g0, gf = len(circuit.gates), len(fused.gates)
+    decision = select_precision(n, gf)
+    from paper_2604_03816_b200.circuit import Precision
+    precision = Precision(prec)
+    opts = plan_options(cost_budget=args.cost_budget, stages=args.stages,
+                        tile_bits=args.tile_bits, min_low_bits=args.min_low_bits)
+    eng = B200Engine("b200-bench", device=local, options=opts)
+
+    if world > 1:
+        from paper_2604_03816_b200.sharded import ShardedEngine
+        return run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world, local)
+
+    plan = eng.plan(fused, precision)
+    n_passes = plan.num_passes
+    state = eng.init_state(n, precision)
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    import ctypes as C
+    from paper_2604_03816_b200 import _native
+    L = _native.lib()
+    pc = prec_code(precision)
+    amp_bytes = precision.amplitude_bytes
+
+    def step(events=None):
+        _native.check(L.svb_fill_basis(C.c_void_p(state.tensor.data_ptr()), n, pc, 0, C.c_void_p(s)))
+        if events is None:
+            plan.execute(state.tensor, s)
+        else:
+            for p in range(n_passes):
+                events[p][0].record(stream)
+                plan.execute(state.tensor, s, p, 1)
+                events[p][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_passes)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    pass_ms = [sum(ev[k][p][0].elapsed_time(ev[k][p][1]) for k in range(args.steps)) / args.steps
+               for p in range(n_passes)]
+    ms_step = total_ms / args.steps
+    value = g0 / (ms_step / 1e3)
+    norm = eng.norm_squared(state)
+
+    # roofline of the dominant kernel (k_tile_pass): algorithmic bytes per launch
+    bytes_per_pass = 2 * (1 << n) * amp_bytes
+    avg_pass_ms = sum(pass_ms) / n_passes
+    achieved = bytes_per_pass / (avg_pass_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peak_hbm()
+    best_pass = min(pass_ms)
+
+    # e2e: public API from a host circuit: plan + launch (kernel-parameter H2D) +
+    # run + device->host read of the result (norm^2 and amplitude 0)
+    eng.release(state)
+    del state
+    torch.cuda.empty_cache()
+    e2e_times = []
+    h2d = n_passes * PASS_ARGS_BYTES  # __grid_constant__ parameter block per launch
+    for k in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = eng.run_circuit(fused, precision)
+        nrm = eng.norm_squared(st)
+        a0 = complex(st.tensor[0].item())
+        dt = time.perf_counter() - t0
+        eng.release(st)
+        del st
+        if k:
+            e2e_times.append(dt)
+    e2e_value = g0 / statistics.median(e2e_times)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        torch.cuda.empty_cache()
+        cpu = cpu_baseline(fused, g0, n, prec, budget_s=20.0)
+
+    line = {
+        "metric": "gates/s", "value": value, "unit": "gates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64" if prec == "single" else "c128", "data": "synthetic seeded circuit",
+        "config": {"workload": f"{cfg}: {kind}-{n} {prec}, fused {g0}->{gf} (width {args.fuse_width})",
+                   "n_qubits": n, "g_original": g0, "g_fused": gf, "passes": n_passes,
+                   "state_bytes": (1 << n) * amp_bytes,
+                   "l2": "state larger than the 126 MB L2; no flush needed",
+                   "precision_decision": decision.rationale + " (bench forces "
+                   + prec + " as BASELINE config names it)",
+                   "circuit_ms": ms_step, "fused_gates_per_s": gf / (ms_step / 1e3),
+                   "passes_per_s": n_passes / (ms_step / 1e3), "norm_after": norm},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_tile_pass", "bytes_per_launch": bytes_per_pass,
+                     "avg_launch_ms": avg_pass_ms, "best_launch_ms": best_pass,
+                     "best_frac": bytes_per_pass / (best_pass / 1e3) / 1e9 / peak},
+        "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 8 + (8 if pc == 0 else 16),
+                "path": "B200Engine.run_circuit(fused circuit) + norm_squared + amplitude[0] read"},
+        "gpu_launches": args.steps * (n_passes + 2),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_sharded(*a, **k):  # filled in by the sharded engine milestone
+    raise SystemExit("sharded bench not implemented yet")
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,122 @@
+/*
+ * svb200.h -- C ABI of the B200 state-vector engine (libsvb200.so).
+ *
+ * The reference package (aqsim, pure Python/NumPy) has no FFI; its plugin
+ * boundary is the Python ``Engine`` class (ref pkg/src/aqsim/engines.py:110-187).
+ * This ABI sits *under* that boundary: the Python ``B200Engine``
+ * (paper_2604_03816_b200/engine.py) binds it with ctypes, and any other host
+ * (C, C++, another FFI) can bind the same symbols.  Each entry point names the
+ * reference symbol whose work it replaces.
+ *
+ * Conventions (identical to the reference):
+ *   - amplitudes are interleaved complex (float2 for SVB_C64, double2 for
+ *     SVB_C128), 2^n_local contiguous elements, little-endian index: bit t of
+ *     the index is (local physical) qubit t;
+ *   - a k-qubit matrix is 2^k x 2^k, row-major, interleaved complex128
+ *     (re, im doubles), and its local bit j acts on targets[j];
+ *     for SVB_C64 states the matrix is rounded to complex64 before use,
+ *     exactly as ref engines.py:157 does;
+ *   - device pointers are borrowed, never freed or reallocated;
+ *   - ``stream`` is a cudaStream_t (NULL = legacy default stream); every call
+ *     is stream-ordered and asynchronous unless it returns host data.
+ *
+ * Errors: every int-returning call returns SVB_OK (0) or a negative status;
+ * svb_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef SVB200_H_
+#define SVB200_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVB_ABI_VERSION 1
+#define SVB_MAX_TARGETS 8   /* per gate; ref allows any k, fusion emits k <= 3 */
+
+enum svb_precision { SVB_C64 = 0, SVB_C128 = 1 };
+
+enum svb_status {
+  SVB_OK = 0,
+  SVB_EINVAL = -1,       /* bad argument      -> Python ValueError        */
+  SVB_ECUDA = -2,        /* CUDA runtime error -> RuntimeError            */
+  SVB_ENOMEM = -3,       /* allocation refused -> AllocationError         */
+  SVB_EUNSUPPORTED = -4  /* shape outside what the kernels support        */
+};
+
+typedef struct svb_plan svb_plan;
+
+/* Planner knobs; zero-initialise for defaults. */
+typedef struct svb_plan_options {
+  int tile_bits;        /* qubits per shared-memory tile (0: 12 for c64, 11 for c128) */
+  int min_low_bits;     /* contiguous low qubits always in the tile (0: 512-B chunks) */
+  int max_ops_per_pass; /* 0: 48 (kernel limit)                                      */
+  double cost_budget;   /* compute budget per pass as a multiple of the pass's HBM
+                           time; 0: default 1.0, <0: unlimited                       */
+  int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
+  int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
+} svb_plan_options;
+
+/* Per-pass description (for tests, profiling and the sharded driver). */
+typedef struct svb_pass_info {
+  int tile_bits;        /* T */
+  int low_bits;         /* L: tile = 2^m chunks of 2^L contiguous amplitudes */
+  int num_high;         /* m */
+  int high[8];          /* physical qubits of tile bits L..L+m-1, ascending */
+  int num_kernel_ops;   /* ops the kernel applies (after diagonal merging) */
+  int num_gates;        /* input gates covered by this pass */
+  double est_cost;      /* planner cost estimate (fraction of HBM time) */
+} svb_pass_info;
+
+int svb_abi_version(void);
+const char* svb_last_error(void);
+
+/* Device facts (needs a GPU). */
+int svb_device_sm_count(int* out);
+
+/* |basis> preparation -- replaces Engine.init_state (ref engines.py:130-140).
+ * Writes 0 everywhere and 1 at index_of_one (pass -1 for an all-zero shard). */
+int svb_fill_basis(void* amps, int n_local, int prec, long long index_of_one, void* stream);
+
+/* One gate, one HBM pass -- replaces Engine.apply_gate -> _apply_single /
+ * _apply_multi (ref engines.py:152-162, kernels 62-105).  Exactly diagonal
+ * matrices take the diagonal kernel path. */
+int svb_apply_gate(void* amps, int n_local, int prec, int k, const int* targets,
+                   const double* matrix, void* stream);
+
+/* Launch plans -- replace the per-gate loop of Engine.run_circuit
+ * (ref engines.py:174-187) for a fused circuit (ref dag.py:177-217 output).
+ * op_k[i] = arity of gate i; op_targets holds SVB_MAX_TARGETS ints per gate
+ * (first op_k[i] used); op_mats concatenates the 2^k x 2^k complex128
+ * matrices (2 * 4^k doubles per gate).  Planning is host-only (no GPU). */
+int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int* op_targets,
+                    const double* op_mats, const svb_plan_options* opts, svb_plan** out);
+int svb_plan_num_passes(const svb_plan* plan);
+int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out);
+/* Input-gate indices of pass `pass`, in the order the kernel applies them. */
+int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap);
+/* Kernel op i of pass `pass`: kind 0 dense / 1 diagonal, tile-local targets,
+ * coefficients as complex128 (dense 4^k, diagonal 2^k entries). */
+int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* tile_targets,
+                       double* coeffs, int coeff_cap);
+int svb_plan_execute(svb_plan* plan, void* amps, void* stream);
+int svb_plan_execute_range(svb_plan* plan, void* amps, int first_pass, int num_passes, void* stream);
+void svb_plan_destroy(svb_plan* plan);
+
+/* FP64-accumulated reductions -- replace StateVector.norm_squared
+ * (ref circuit.py:200-201) and the overlap inside state_fidelity
+ * (ref engines.py:340-346).  Results are written to host memory; the call
+ * synchronises `stream`.  out2 = {re, im} of sum conj(a[i]) * b[i]. */
+int svb_dot(const void* a, const void* b, int n_local, int prec, double* out2, void* stream);
+int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream);
+
+/* |amp|^2 as float64 -- replaces StateVector.probabilities (ref circuit.py:203-205)
+ * for a slice [offset, offset+count) of the shard. */
+int svb_probabilities(const void* amps, int prec, long long offset, long long count,
+                      double* out_device, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVB200_H_ */

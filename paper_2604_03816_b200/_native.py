@@ -1,0 +1,172 @@
+"""ctypes binding of libsvb200.so (the C ABI in include/svb200.h).
+
+There is no fallback: if the shared library is missing or fails to load,
+every entry point raises.  Planning calls (``plan_*``) are host-only and work
+without a GPU; everything that touches amplitudes needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsvb200.so")
+
+SVB_C64, SVB_C128 = 0, 1
+SVB_OK, SVB_EINVAL, SVB_ECUDA, SVB_ENOMEM, SVB_EUNSUPPORTED = 0, -1, -2, -3, -4
+SVB_MAX_TARGETS = 8
+ABI_VERSION = 1
+
+# every symbol declared in include/svb200.h (tests check the library exports them)
+EXPORTS = (
+    "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
+    "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
+    "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_execute",
+    "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
+    "svb_probabilities",
+)
+
+
+class PlanOptions(C.Structure):
+    _fields_ = [("tile_bits", C.c_int), ("min_low_bits", C.c_int),
+                ("max_ops_per_pass", C.c_int), ("cost_budget", C.c_double),
+                ("no_diag_merge", C.c_int), ("stages", C.c_int)]
+
+
+class PassInfo(C.Structure):
+    _fields_ = [("tile_bits", C.c_int), ("low_bits", C.c_int), ("num_high", C.c_int),
+                ("high", C.c_int * 8), ("num_kernel_ops", C.c_int), ("num_gates", C.c_int),
+                ("est_cost", C.c_double)]
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        super().__init__(f"libsvb200 error {code}: {msg}")
+
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the library; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2604_03816_b200._build` "
+            "(the B200 engine has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i, ll, d = C.c_void_p, C.c_int, C.c_longlong, C.c_double
+    ip, dp = C.POINTER(C.c_int), C.POINTER(C.c_double)
+    sig = {
+        "svb_abi_version": (i, []),
+        "svb_last_error": (C.c_char_p, []),
+        "svb_device_sm_count": (i, [ip]),
+        "svb_fill_basis": (i, [vp, i, i, ll, vp]),
+        "svb_apply_gate": (i, [vp, i, i, i, ip, dp, vp]),
+        "svb_plan_create": (i, [i, i, i, ip, ip, dp, C.POINTER(PlanOptions), C.POINTER(vp)]),
+        "svb_plan_num_passes": (i, [vp]),
+        "svb_plan_pass_info": (i, [vp, i, C.POINTER(PassInfo)]),
+        "svb_plan_pass_gates": (i, [vp, i, ip, i]),
+        "svb_plan_kernel_op": (i, [vp, i, i, ip, ip, ip, dp, i]),
+        "svb_plan_execute": (i, [vp, vp, vp]),
+        "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
+        "svb_plan_destroy": (None, [vp]),
+        "svb_dot": (i, [vp, vp, i, i, dp, vp]),
+        "svb_norm2": (i, [vp, i, i, dp, vp]),
+        "svb_probabilities": (i, [vp, i, ll, ll, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    if L.svb_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"libsvb200 ABI {L.svb_abi_version()} != expected {ABI_VERSION}")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> int:
+    if rc < 0:
+        msg = lib().svb_last_error().decode(errors="replace")
+        if rc == SVB_EINVAL:
+            raise ValueError(msg)
+        raise NativeError(rc, msg)
+    return rc
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class NativePlan:
+    """Owns an ``svb_plan*``; host-side only until ``execute``."""
+
+    def __init__(self, n_local: int, prec: int, ks: np.ndarray, targets: np.ndarray,
+                 mats: np.ndarray, options: PlanOptions | None = None):
+        self._h = None
+        self.n_local = n_local
+        self.prec = prec
+        self.num_gates = int(ks.size)
+        ks = np.ascontiguousarray(ks, dtype=np.int32)
+        targets = np.ascontiguousarray(targets, dtype=np.int32)
+        mats = np.ascontiguousarray(mats, dtype=np.float64)
+        h = C.c_void_p()
+        opt = C.byref(options) if options is not None else None
+        check(lib().svb_plan_create(n_local, prec, int(ks.size), _iptr(ks), _iptr(targets),
+                                    _dptr(mats), opt, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def num_passes(self) -> int:
+        return check(lib().svb_plan_num_passes(self._h))
+
+    def pass_info(self, p: int) -> dict:
+        info = PassInfo()
+        check(lib().svb_plan_pass_info(self._h, p, C.byref(info)))
+        return {"tile_bits": info.tile_bits, "low_bits": info.low_bits,
+                "high": [info.high[b] for b in range(info.num_high)],
+                "num_kernel_ops": info.num_kernel_ops, "num_gates": info.num_gates,
+                "est_cost": info.est_cost}
+
+    def pass_gates(self, p: int) -> list[int]:
+        buf = np.zeros(max(1, self.num_gates), dtype=np.int32)
+        n = check(lib().svb_plan_pass_gates(self._h, p, _iptr(buf), int(buf.size)))
+        return [int(x) for x in buf[:n]]
+
+    def kernel_op(self, p: int, i: int) -> dict:
+        kind, k = C.c_int(), C.c_int()
+        tg = np.zeros(SVB_MAX_TARGETS, dtype=np.int32)
+        co = np.zeros(2 * 4096, dtype=np.float64)
+        n = check(lib().svb_plan_kernel_op(self._h, p, i, C.byref(kind), C.byref(k), _iptr(tg),
+                                           _dptr(co), 4096))
+        coeffs = co[:2 * n].view(np.complex128).copy()
+        return {"kind": "diag" if kind.value == 1 else "dense", "k": k.value,
+                "targets": [int(t) for t in tg[:k.value]], "coeffs": coeffs}
+
+    def execute(self, amps_ptr: int, stream: int, first: int = 0, count: int | None = None):
+        if count is None:
+            count = self.num_passes() - first
+        check(lib().svb_plan_execute_range(self._h, C.c_void_p(amps_ptr), first, count,
+                                           C.c_void_p(stream)))
+
+    def close(self):
+        if self._h is not None and _lib is not None:
+            _lib.svb_plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass

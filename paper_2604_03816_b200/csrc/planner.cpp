@@ -1,0 +1,353 @@
+// Native launch planner (see planner.h).  Host-only C++: runs without a GPU,
+// which is what lets the CPU test-suite check plan legality against the oracle.
+#include "planner.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace svb {
+
+int default_tile_bits(int prec) { return prec == SVB_C64 ? 12 : 11; }
+int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
+
+namespace {
+
+// ---------------------------------------------------------------- cost model
+// Per-amplitude SM cycles, normalised by the pass's HBM time.  B200: HBM
+// ~6.5 TB/s over 148 SMs at ~1.9 GHz = ~23 B/clk/SM; FP32 FMA 128/clk/SM,
+// FP64 FMA 64/clk/SM; shared memory 128 B/clk/SM.  A pass is HBM-bound while
+// the summed op cost stays below 1.0 (the default budget).
+struct CostModel {
+  double s, fma, mem;
+  explicit CostModel(int prec) {
+    s = prec == SVB_C64 ? 8.0 : 16.0;
+    fma = prec == SVB_C64 ? 128.0 : 64.0;
+    mem = 2.0 * s / 23.0;
+  }
+  double dense(int k) const {
+    double flops = 4.0 * double(1 << k) / fma;
+    double smem = 2.0 * s / 128.0 + (k >= 3 ? double(1 << k) * s / 128.0 / 8.0 : 0.0);
+    return (std::max(flops, smem) * 1.15 + 0.02) / mem;
+  }
+  double diag(int k) const {
+    double flops = 4.0 / fma + 2.0 * k / 64.0;
+    double smem = 3.0 * s / 128.0;
+    return (std::max(flops, smem) * 1.15 + 0.02) / mem;
+  }
+  double of(const Gate& g) const { return g.diag ? diag(g.k) : dense(g.k); }
+};
+
+bool is_diagonal(int k, const double* mat) {
+  const int d = 1 << k;
+  for (int r = 0; r < d; ++r)
+    for (int c = 0; c < d; ++c)
+      if (r != c && (mat[2 * (r * d + c)] != 0.0 || mat[2 * (r * d + c) + 1] != 0.0)) return false;
+  return true;
+}
+
+// Extract the bits of `x` at positions pos[0..n) into a compact index.
+inline int gather_bits(int x, const int* pos, int n) {
+  int r = 0;
+  for (int b = 0; b < n; ++b) r |= ((x >> pos[b]) & 1) << b;
+  return r;
+}
+
+// Running product of diagonal gates over a growing bit set (tile-local bits).
+struct DiagAcc {
+  std::vector<int> bits;   // sorted tile-local positions
+  std::vector<cd> table{cd(1.0, 0.0)};
+  std::vector<int> gates;
+  bool empty() const { return gates.empty(); }
+
+  int union_size(const int* tg, int k) const {
+    std::vector<int> u(bits);
+    for (int j = 0; j < k; ++j)
+      if (std::find(u.begin(), u.end(), tg[j]) == u.end()) u.push_back(tg[j]);
+    return int(u.size());
+  }
+  void absorb(const int* tg, int k, const std::vector<cd>& d, int gate) {
+    std::vector<int> nb(bits);
+    for (int j = 0; j < k; ++j)
+      if (std::find(nb.begin(), nb.end(), tg[j]) == nb.end()) nb.push_back(tg[j]);
+    std::sort(nb.begin(), nb.end());
+    // positions of old bits / gate bits inside the new compact index
+    std::vector<int> old_pos(bits.size()), g_pos(k);
+    for (size_t i = 0; i < bits.size(); ++i)
+      old_pos[i] = int(std::find(nb.begin(), nb.end(), bits[i]) - nb.begin());
+    for (int j = 0; j < k; ++j) g_pos[j] = int(std::find(nb.begin(), nb.end(), tg[j]) - nb.begin());
+    std::vector<cd> nt(size_t(1) << nb.size());
+    for (size_t u = 0; u < nt.size(); ++u) {
+      int oi = gather_bits(int(u), old_pos.data(), int(old_pos.size()));
+      int gi = gather_bits(int(u), g_pos.data(), k);
+      nt[u] = table[oi] * d[gi];
+    }
+    bits.swap(nb);
+    table.swap(nt);
+    gates.push_back(gate);
+  }
+  bool touches(const int* tg, int k) const {
+    for (int j = 0; j < k; ++j)
+      if (std::find(bits.begin(), bits.end(), tg[j]) != bits.end()) return true;
+    return false;
+  }
+  KernelOp take() {
+    KernelOp op;
+    op.kind = OP_DIAG;
+    op.k = int(bits.size());
+    for (int j = 0; j < op.k; ++j) op.tgt[j] = bits[j];
+    op.coeff = table;
+    op.gates = gates;
+    *this = DiagAcc();
+    return op;
+  }
+};
+
+size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
+
+}  // namespace
+
+bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const double* op_mats,
+                std::vector<Gate>& out, std::string& err) {
+  out.clear();
+  out.reserve(n_ops);
+  size_t off = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    Gate g;
+    g.k = op_k[i];
+    if (g.k < 1 || g.k > kMaxDenseK) {
+      err = "gate " + std::to_string(i) + ": arity " + std::to_string(g.k) +
+            " outside supported range 1.." + std::to_string(kMaxDenseK);
+      return false;
+    }
+    if (g.k > n) {
+      err = "gate " + std::to_string(i) + ": arity exceeds qubit count";
+      return false;
+    }
+    for (int j = 0; j < g.k; ++j) {
+      int t = op_targets[i * SVB_MAX_TARGETS + j];
+      if (t < 0 || t >= n) {
+        err = "target out of range for " + std::to_string(n) + " qubits at gate " + std::to_string(i);
+        return false;
+      }
+      for (int j2 = 0; j2 < j; ++j2)
+        if (g.t[j2] == t) {
+          err = "duplicate target at gate " + std::to_string(i);
+          return false;
+        }
+      g.t[j] = t;
+    }
+    const int d = 1 << g.k;
+    const double* mat = op_mats + off;
+    off += size_t(2) * d * d;
+    g.diag = is_diagonal(g.k, mat);
+    if (g.diag) {
+      g.m.resize(d);
+      for (int r = 0; r < d; ++r) g.m[r] = cd(mat[2 * (r * d + r)], mat[2 * (r * d + r) + 1]);
+    } else {
+      g.m.resize(size_t(d) * d);
+      for (int e = 0; e < d * d; ++e) g.m[e] = cd(mat[2 * e], mat[2 * e + 1]);
+    }
+    out.push_back(std::move(g));
+  }
+  return true;
+}
+
+bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_options& opt_in,
+                Plan& plan, std::string& err) {
+  if (n < 1 || n > 62) {
+    err = "n_local must be in 1..62";
+    return false;
+  }
+  if (prec != SVB_C64 && prec != SVB_C128) {
+    err = "precision must be SVB_C64 or SVB_C128";
+    return false;
+  }
+  svb_plan_options opt = opt_in;
+  int T = opt.tile_bits > 0 ? opt.tile_bits : default_tile_bits(prec);
+  if (T > 13) T = 13;
+  if (T > n) T = n;
+  int Lmin = opt.min_low_bits > 0 ? opt.min_low_bits : default_min_low_bits(prec);
+  if (Lmin > T) Lmin = T;
+  if (Lmin < T - kMaxHigh) Lmin = T - kMaxHigh;
+  if (prec == SVB_C64 && Lmin < 1) Lmin = 1;  // chunks must be >= 16 bytes
+  const int mmax = T - Lmin;
+  const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
+                          ? opt.max_ops_per_pass : kMaxOps;
+  const double budget = opt.cost_budget == 0.0 ? 1.0 : opt.cost_budget;
+  const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
+  const CostModel cm(prec);
+
+  plan.n = n;
+  plan.prec = prec;
+  plan.opt = opt;
+  plan.passes.clear();
+
+  for (size_t i = 0; i < gates.size(); ++i) {
+    int high_needed = 0;
+    for (int j = 0; j < gates[i].k; ++j) high_needed += gates[i].t[j] >= Lmin;
+    if (high_needed > mmax) {
+      err = "gate " + std::to_string(i) + " needs more strided tile bits than the tile allows";
+      return false;
+    }
+  }
+
+  std::vector<int> pending(gates.size());
+  for (size_t i = 0; i < gates.size(); ++i) pending[i] = int(i);
+
+  while (!pending.empty()) {
+    std::vector<char> block_all(n, 0), block_dense(n, 0), in_high(n, 0);
+    int n_high = 0;
+    double cost = 0.0;
+    std::vector<int> taken, deferred;
+    // Mirror of the diagonal-run merge done at lowering time, so that a
+    // diagonal gate joining an open run is charged only its marginal cost and
+    // the coefficient pool is accounted for with the merged table sizes.
+    std::vector<int> acc_bits;
+    bool acc_open = false;
+    size_t closed_pool = 0;
+    const bool merging = !opt.no_diag_merge;
+    for (int gi : pending) {
+      const Gate& g = gates[gi];
+      bool blocked = false;
+      for (int j = 0; j < g.k && !blocked; ++j)
+        blocked = block_all[g.t[j]] || (!g.diag && block_dense[g.t[j]]);
+      bool take = false;
+      if (!blocked) {
+        int extra = 0;
+        for (int j = 0; j < g.k; ++j) extra += (g.t[j] >= Lmin && !in_high[g.t[j]]);
+        double c;
+        size_t new_closed = closed_pool;
+        std::vector<int> new_acc = acc_bits;
+        bool new_open = acc_open;
+        if (!merging) {
+          c = cm.of(g);
+          new_closed += g.m.size();
+        } else if (g.diag) {
+          std::vector<int> u = acc_bits;
+          for (int j = 0; j < g.k; ++j)
+            if (std::find(u.begin(), u.end(), g.t[j]) == u.end()) u.push_back(g.t[j]);
+          if (acc_open && int(u.size()) <= kMaxDiagK) {
+            c = cm.diag(int(u.size())) - cm.diag(int(acc_bits.size()));
+            new_acc = u;
+          } else {
+            if (acc_open) new_closed += size_t(1) << acc_bits.size();
+            c = cm.diag(g.k);
+            new_acc.assign(g.t, g.t + g.k);
+          }
+          new_open = true;
+        } else {
+          c = cm.dense(g.k);
+          new_closed += g.m.size();
+          bool touches = false;
+          for (int j = 0; j < g.k; ++j)
+            touches |= std::find(acc_bits.begin(), acc_bits.end(), g.t[j]) != acc_bits.end();
+          if (acc_open && touches) {
+            new_closed += size_t(1) << acc_bits.size();
+            new_acc.clear();
+            new_open = false;
+          }
+        }
+        const size_t new_pool = new_closed + (new_open ? (size_t(1) << new_acc.size()) : 0);
+        take = n_high + extra <= mmax && int(taken.size()) < max_ops && new_pool <= pool_cap &&
+               (taken.empty() || budget < 0 || cost + c <= budget);
+        if (take) {
+          for (int j = 0; j < g.k; ++j)
+            if (g.t[j] >= Lmin && !in_high[g.t[j]]) {
+              in_high[g.t[j]] = 1;
+              ++n_high;
+            }
+          cost += c;
+          closed_pool = new_closed;
+          acc_bits = new_acc;
+          acc_open = new_open;
+          taken.push_back(gi);
+        }
+      }
+      if (!take) {
+        deferred.push_back(gi);
+        for (int j = 0; j < g.k; ++j) (g.diag ? block_dense : block_all)[g.t[j]] = 1;
+      }
+    }
+
+    // ---- tile qubit set: low Lmin qubits + chosen high ones, filled upward
+    Pass p;
+    p.T = T;
+    std::vector<char> inq(n, 0);
+    for (int q = 0; q < Lmin; ++q) inq[q] = 1;
+    int cnt = Lmin;
+    for (int q = Lmin; q < n; ++q)
+      if (in_high[q]) {
+        inq[q] = 1;
+        ++cnt;
+      }
+    for (int q = 0; q < n && cnt < T; ++q)
+      if (!inq[q]) {
+        inq[q] = 1;
+        ++cnt;
+      }
+    int L = 0;
+    while (L < n && inq[L]) ++L;
+    if (L > T) L = T;
+    p.L = L;
+    p.m = 0;
+    for (int q = L; q < n; ++q)
+      if (inq[q]) p.high[p.m++] = q;
+    if (p.L + p.m != T || p.m > kMaxHigh) {
+      err = "internal planner error: tile set";
+      return false;
+    }
+    auto local = [&](int q) {
+      if (q < p.L) return q;
+      for (int b = 0; b < p.m; ++b)
+        if (p.high[b] == q) return p.L + b;
+      return -1;
+    };
+
+    // ---- lower to kernel ops, merging diagonal runs
+    auto lower_plain = [&](int gi) {
+      const Gate& g = gates[gi];
+      KernelOp op;
+      op.kind = g.diag ? OP_DIAG : OP_DENSE;
+      op.k = g.k;
+      for (int j = 0; j < g.k; ++j) op.tgt[j] = local(g.t[j]);
+      op.coeff = g.m;
+      op.gates.push_back(gi);
+      return op;
+    };
+    std::vector<KernelOp> ops;
+    bool merge = !opt.no_diag_merge;
+    if (merge) {
+      DiagAcc acc;
+      for (int gi : taken) {
+        const Gate& g = gates[gi];
+        int tg[kMaxK];
+        for (int j = 0; j < g.k; ++j) tg[j] = local(g.t[j]);
+        if (g.diag) {
+          if (!acc.empty() && acc.union_size(tg, g.k) > kMaxDiagK) ops.push_back(acc.take());
+          acc.absorb(tg, g.k, g.m, gi);
+        } else {
+          if (!acc.empty() && acc.touches(tg, g.k)) ops.push_back(acc.take());
+          ops.push_back(lower_plain(gi));
+        }
+      }
+      if (!acc.empty()) ops.push_back(acc.take());
+      size_t used = 0;
+      for (auto& o : ops) used += coeff_elems(o);
+      if (used > pool_cap) merge = false;  // merged tables grew past the pool
+    }
+    if (!merge) {
+      ops.clear();
+      for (int gi : taken) ops.push_back(lower_plain(gi));
+    }
+    p.ops = std::move(ops);
+    p.num_gates = int(taken.size());
+    p.cost = 0.0;
+    for (auto& o : p.ops) p.cost += o.kind == OP_DIAG ? cm.diag(o.k) : cm.dense(o.k);
+    plan.passes.push_back(std::move(p));
+    pending.swap(deferred);
+  }
+  return true;
+}
+
+}  // namespace svb

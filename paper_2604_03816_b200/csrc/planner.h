@@ -1,0 +1,63 @@
+// Native launch planner: lowers a (fused) gate list into tile passes.
+//
+// Input is the output of the DAG fusion pass (ref pkg/src/aqsim/dag.py:177-217:
+// CUSTOM ops on an ascending qubit union, or named gates), one matrix per gate.
+// Output is a sequence of passes; each pass is one launch of the tile kernel
+// and one HBM round trip of the state.  The reference applies one gate per
+// whole-array sweep (ref engines.py:182-185); here every gate whose qubits fit
+// the pass's tile qubit set, and that no deferred gate must precede, joins the
+// pass (diagonal gates commute with each other and are merged into one table).
+#pragma once
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "svb200.h"
+#include "svb_types.h"
+
+namespace svb {
+
+using cd = std::complex<double>;
+
+struct Gate {
+  int k = 0;
+  int t[kMaxK] = {0};
+  bool diag = false;
+  std::vector<cd> m;  // dense: 2^k x 2^k row-major; diagonal: the 2^k diagonal entries
+};
+
+struct KernelOp {
+  int kind = OP_DENSE;
+  int k = 0;
+  int tgt[kMaxK] = {0};    // tile-local bits, matrix-local bit j -> tgt[j]
+  std::vector<cd> coeff;
+  std::vector<int> gates;  // input gates folded into this op, program order
+};
+
+struct Pass {
+  int T = 0, L = 0, m = 0;
+  int high[kMaxHigh] = {0};
+  std::vector<KernelOp> ops;
+  double cost = 0.0;
+  int num_gates = 0;
+};
+
+struct Plan {
+  int n = 0;
+  int prec = SVB_C128;
+  svb_plan_options opt{};
+  std::vector<Pass> passes;
+};
+
+// Tile defaults per precision: 32 KiB tiles, 512-byte contiguous chunks.
+int default_tile_bits(int prec);
+int default_min_low_bits(int prec);
+
+// Parse + classify the raw ABI arrays into gates (diagonal detection).
+bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const double* op_mats,
+                std::vector<Gate>& out, std::string& err);
+
+bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_options& opt,
+                Plan& out, std::string& err);
+
+}  // namespace svb

@@ -1,0 +1,368 @@
+// extern "C" entry points of libsvb200.so (declared in include/svb200.h).
+//
+// Thin host layer: argument validation, plan objects (planner.cpp) turned
+// into __grid_constant__ kernel parameter blocks, launch geometry (persistent
+// grid = SMs x resident CTAs), error mapping.  No device memory is owned by a
+// plan; reductions use stream-ordered scratch (cudaMallocAsync).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "planner.h"
+#include "svb200.h"
+#include "svb_kernels.cuh"
+
+using namespace svb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SVB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define SVB_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+bool valid_prec(int p) { return p == SVB_C64 || p == SVB_C128; }
+
+struct DeviceFacts {
+  int sm_count = 0;
+  int ctas_per_sm_c64 = 0;
+  int ctas_per_sm_c128 = 0;
+  bool attrs_set = false;
+};
+std::mutex g_dev_mu;
+DeviceFacts g_dev[64];
+
+int device_facts(DeviceFacts** out) {
+  int dev = 0;
+  SVB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(SVB_EUNSUPPORTED, "device index out of range");
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceFacts& f = g_dev[dev];
+  if (!f.attrs_set) {
+    SVB_CUDA(cudaDeviceGetAttribute(&f.sm_count, cudaDevAttrMultiProcessorCount, dev));
+    int max_optin = 0;
+    SVB_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const void* fns[] = {(const void*)k_tile_pass<float2, 2>, (const void*)k_tile_pass<float2, 3>,
+                         (const void*)k_tile_pass<float2, 6>, (const void*)k_tile_pass<double2, 2>,
+                         (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>};
+    for (const void* fn : fns)
+      SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    f.attrs_set = true;
+  }
+  *out = &f;
+  return SVB_OK;
+}
+
+template <class C>
+void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
+  std::memset(&a.h, 0, sizeof(a.h));
+  a.h.T = p.T;
+  a.h.L = p.L;
+  a.h.m = p.m;
+  a.h.n_ops = int(p.ops.size());
+  for (int b = 0; b < p.m; ++b) a.h.high[b] = p.high[b];
+  a.h.stages = stages;
+  int off = 0;
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    const KernelOp& ko = p.ops[i];
+    OpDesc& d = a.ops[i];
+    std::memset(&d, 0, sizeof(d));
+    d.kind = ko.kind;
+    d.k = ko.k;
+    d.coeff_off = off;
+    for (int j = 0; j < ko.k; ++j) d.tgt[j] = d.srt[j] = ko.tgt[j];
+    std::sort(d.srt, d.srt + ko.k);
+    for (const cd& z : ko.coeff) {
+      a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
+      a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
+      ++off;
+    }
+  }
+  a.h.coeff_count = off;
+}
+
+}  // namespace
+
+struct svb_plan {
+  Plan plan;
+  int stages = 3;
+  std::vector<PassArgs<float2>> args64;
+  std::vector<PassArgs<double2>> args128;
+};
+
+namespace {
+
+template <class C>
+int launch_pass(const PassArgs<C>& a0, int n_local, C* amps, cudaStream_t stream) {
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  const PassArgs<C>& a = a0;
+  const size_t smem = tile_pass_smem_bytes<C>(a.h);
+  int kmax = 0;
+  for (int i = 0; i < a.h.n_ops; ++i)
+    if (a.ops[i].kind == OP_DENSE) kmax = std::max(kmax, a.ops[i].k);
+  void (*fn)(C*, PassArgs<C>) = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
+  int per_sm = 0;
+  SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+  if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tile pass does not fit on an SM (shared memory)");
+  const long long n_tiles = a.h.n_tiles;
+  long long grid = std::min<long long>(n_tiles, (long long)f->sm_count * per_sm);
+  if (grid < 1) grid = 1;
+  fn<<<(unsigned)grid, kThreads, smem, stream>>>(amps, a);
+  SVB_CUDA(cudaGetLastError());
+  (void)n_local;
+  return SVB_OK;
+}
+
+template <class C>
+int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int first, int count, cudaStream_t s) {
+  for (int i = first; i < first + count; ++i) {
+    int rc = launch_pass<C>(args[i], p->plan.n, static_cast<C*>(amps), s);
+    if (rc) return rc;
+  }
+  return SVB_OK;
+}
+
+template <class C>
+int dot_impl(const void* a, const void* b, long long n, double* out2, cudaStream_t s) {
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  const int threads = 512;
+  long long grid = std::min<long long>((n + threads - 1) / threads, (long long)f->sm_count * 4);
+  if (grid < 1) grid = 1;
+  double2* partial = nullptr;
+  SVB_CUDA(cudaMallocAsync(&partial, sizeof(double2) * grid, s));
+  k_dot<C><<<(unsigned)grid, threads, 0, s>>>(static_cast<const C*>(a), static_cast<const C*>(b), n, partial);
+  cudaError_t le = cudaGetLastError();
+  std::vector<double2> host(grid);
+  cudaError_t ce = le == cudaSuccess
+                       ? cudaMemcpyAsync(host.data(), partial, sizeof(double2) * grid, cudaMemcpyDeviceToHost, s)
+                       : le;
+  cudaFreeAsync(partial, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "svb_dot");
+  SVB_CUDA(cudaStreamSynchronize(s));
+  double re = 0.0, im = 0.0;
+  for (long long i = 0; i < grid; ++i) {
+    re += host[i].x;
+    im += host[i].y;
+  }
+  out2[0] = re;
+  out2[1] = im;
+  return SVB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int svb_abi_version(void) { return SVB_ABI_VERSION; }
+
+const char* svb_last_error(void) { return g_err.c_str(); }
+
+int svb_device_sm_count(int* out) {
+  if (!out) return fail(SVB_EINVAL, "null out");
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  *out = f->sm_count;
+  return SVB_OK;
+}
+
+int svb_fill_basis(void* amps, int n_local, int prec, long long index_of_one, void* stream) {
+  if (!amps) return fail(SVB_EINVAL, "null amplitudes");
+  if (n_local < 1 || n_local > 62) return fail(SVB_EINVAL, "num_qubits must be >= 1");
+  if (!valid_prec(prec)) return fail(SVB_EINVAL, "bad precision");
+  const long long n = 1LL << n_local;
+  if (index_of_one >= n) return fail(SVB_EINVAL, "index_of_one outside the shard");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  const long long words = n * (prec == SVB_C64 ? 8 : 16) / 16;
+  long long grid = std::min<long long>((words + 255) / 256, (long long)f->sm_count * 8);
+  if (grid < 1) grid = 1;
+  if (prec == SVB_C64) {
+    k_fill_zero<float2><<<(unsigned)grid, 256, 0, s>>>(static_cast<float2*>(amps), n);
+    if (index_of_one >= 0) k_set_one<float2><<<1, 1, 0, s>>>(static_cast<float2*>(amps), index_of_one);
+  } else {
+    k_fill_zero<double2><<<(unsigned)grid, 256, 0, s>>>(static_cast<double2*>(amps), n);
+    if (index_of_one >= 0) k_set_one<double2><<<1, 1, 0, s>>>(static_cast<double2*>(amps), index_of_one);
+  }
+  SVB_CUDA(cudaGetLastError());
+  return SVB_OK;
+}
+
+int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int* op_targets,
+                    const double* op_mats, const svb_plan_options* opts, svb_plan** out) {
+  if (!out) return fail(SVB_EINVAL, "null out");
+  *out = nullptr;
+  if (n_local < 1) return fail(SVB_EINVAL, "num_qubits must be >= 1");
+  if (!valid_prec(prec)) return fail(SVB_EINVAL, "bad precision");
+  if (n_ops < 0 || (n_ops > 0 && (!op_k || !op_targets || !op_mats)))
+    return fail(SVB_EINVAL, "bad gate arrays");
+  svb_plan_options o{};
+  if (opts) o = *opts;
+  std::vector<Gate> gates;
+  std::string err;
+  if (!make_gates(n_local, n_ops, op_k, op_targets, op_mats, gates, err)) return fail(SVB_EINVAL, err);
+  std::unique_ptr<svb_plan> p(new svb_plan());
+  if (!build_plan(n_local, prec, gates, o, p->plan, err)) return fail(SVB_EUNSUPPORTED, err);
+  p->stages = o.stages > 0 ? std::min(o.stages, 6) : 3;
+  const int np = int(p->plan.passes.size());
+  const long long n_tiles = 1LL << (n_local - (np ? p->plan.passes[0].T : 0));
+  if (prec == SVB_C64) {
+    p->args64.resize(np);
+    for (int i = 0; i < np; ++i) {
+      fill_args<float2>(p->plan.passes[i], p->stages, p->args64[i]);
+      p->args64[i].h.n_tiles = n_tiles;
+    }
+  } else {
+    p->args128.resize(np);
+    for (int i = 0; i < np; ++i) {
+      fill_args<double2>(p->plan.passes[i], p->stages, p->args128[i]);
+      p->args128[i].h.n_tiles = n_tiles;
+    }
+  }
+  *out = p.release();
+  return SVB_OK;
+}
+
+int svb_plan_num_passes(const svb_plan* plan) {
+  if (!plan) return fail(SVB_EINVAL, "null plan");
+  return int(plan->plan.passes.size());
+}
+
+int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out) {
+  if (!plan || !out) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  std::memset(out, 0, sizeof(*out));
+  out->tile_bits = p.T;
+  out->low_bits = p.L;
+  out->num_high = p.m;
+  for (int b = 0; b < p.m; ++b) out->high[b] = p.high[b];
+  out->num_kernel_ops = int(p.ops.size());
+  out->num_gates = p.num_gates;
+  out->est_cost = p.cost;
+  return SVB_OK;
+}
+
+int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap) {
+  if (!plan || !out) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  int w = 0;
+  for (const KernelOp& op : plan->plan.passes[pass].ops)
+    for (int g : op.gates) {
+      if (w >= cap) return fail(SVB_EINVAL, "output capacity too small");
+      out[w++] = g;
+    }
+  return w;
+}
+
+int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* tile_targets,
+                       double* coeffs, int coeff_cap) {
+  if (!plan || !kind || !k || !tile_targets) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (i < 0 || i >= int(p.ops.size())) return fail(SVB_EINVAL, "op index out of range");
+  const KernelOp& op = p.ops[i];
+  *kind = op.kind;
+  *k = op.k;
+  for (int j = 0; j < op.k; ++j) tile_targets[j] = op.tgt[j];
+  if (coeffs) {
+    if (int(op.coeff.size()) > coeff_cap) return fail(SVB_EINVAL, "coefficient capacity too small");
+    for (size_t e = 0; e < op.coeff.size(); ++e) {
+      coeffs[2 * e] = op.coeff[e].real();
+      coeffs[2 * e + 1] = op.coeff[e].imag();
+    }
+  }
+  return int(op.coeff.size());
+}
+
+int svb_plan_execute_range(svb_plan* plan, void* amps, int first_pass, int num_passes, void* stream) {
+  if (!plan || !amps) return fail(SVB_EINVAL, "null argument");
+  const int np = int(plan->plan.passes.size());
+  if (first_pass < 0 || num_passes < 0 || first_pass + num_passes > np)
+    return fail(SVB_EINVAL, "pass range out of bounds");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (plan->plan.prec == SVB_C64) return exec_range<float2>(plan, plan->args64, amps, first_pass, num_passes, s);
+  return exec_range<double2>(plan, plan->args128, amps, first_pass, num_passes, s);
+}
+
+int svb_plan_execute(svb_plan* plan, void* amps, void* stream) {
+  if (!plan) return fail(SVB_EINVAL, "null plan");
+  return svb_plan_execute_range(plan, amps, 0, int(plan->plan.passes.size()), stream);
+}
+
+void svb_plan_destroy(svb_plan* plan) { delete plan; }
+
+int svb_apply_gate(void* amps, int n_local, int prec, int k, const int* targets, const double* matrix,
+                   void* stream) {
+  if (!amps || !targets || !matrix) return fail(SVB_EINVAL, "null argument");
+  if (k < 1 || k > SVB_MAX_TARGETS) return fail(SVB_EINVAL, "bad arity");
+  int tg[SVB_MAX_TARGETS] = {0};
+  for (int j = 0; j < k; ++j) tg[j] = targets[j];
+  svb_plan* p = nullptr;
+  int rc = svb_plan_create(n_local, prec, 1, &k, tg, matrix, nullptr, &p);
+  if (rc) return rc;
+  rc = svb_plan_execute(p, amps, stream);
+  svb_plan_destroy(p);
+  return rc;
+}
+
+int svb_dot(const void* a, const void* b, int n_local, int prec, double* out2, void* stream) {
+  if (!a || !b || !out2) return fail(SVB_EINVAL, "null argument");
+  if (n_local < 0 || n_local > 62 || !valid_prec(prec)) return fail(SVB_EINVAL, "bad shape");
+  const long long n = 1LL << n_local;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return prec == SVB_C64 ? dot_impl<float2>(a, b, n, out2, s) : dot_impl<double2>(a, b, n, out2, s);
+}
+
+int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream) {
+  if (!out) return fail(SVB_EINVAL, "null argument");
+  double z[2];
+  int rc = svb_dot(a, a, n_local, prec, z, stream);
+  if (rc) return rc;
+  *out = z[0];
+  return SVB_OK;
+}
+
+int svb_probabilities(const void* amps, int prec, long long offset, long long count, double* out_device,
+                      void* stream) {
+  if (!amps || !out_device || offset < 0 || count < 0) return fail(SVB_EINVAL, "bad argument");
+  if (!valid_prec(prec)) return fail(SVB_EINVAL, "bad precision");
+  if (count == 0) return SVB_OK;
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  long long grid = std::min<long long>((count + 255) / 256, (long long)f->sm_count * 8);
+  if (prec == SVB_C64)
+    k_probabilities<float2><<<(unsigned)grid, 256, 0, s>>>(static_cast<const float2*>(amps) + offset, count,
+                                                            out_device);
+  else
+    k_probabilities<double2><<<(unsigned)grid, 256, 0, s>>>(static_cast<const double2*>(amps) + offset, count,
+                                                             out_device);
+  SVB_CUDA(cudaGetLastError());
+  return SVB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,360 @@
+// sm_100a device code of the B200 state-vector engine.
+//
+// k_tile_pass -- the workhorse: one launch = one HBM pass over the local state
+// applying every kernel op of a planned pass (replaces the per-gate numpy
+// sweeps of ref engines.py:62-105).  Persistent CTAs (one per SM) walk the
+// tiles; a dedicated producer warp moves each tile HBM -> shared memory with
+// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx, SASS UBLKCP) into
+// a ring of `stages` buffers and writes finished tiles back with bulk stores,
+// while 8 compute warps apply the ops in shared memory.  Loads of tile i+1..
+// i+S-1 and the store of tile i-1 overlap the math on tile i.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "svb_types.h"
+
+namespace svb {
+
+// ------------------------------------------------------------------ PTX glue
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void compute_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ------------------------------------------------------------ complex math
+__device__ __forceinline__ float2 cfma(float2 m, float2 v, float2 acc) {
+  acc.x = fmaf(m.x, v.x, acc.x);
+  acc.x = fmaf(-m.y, v.y, acc.x);
+  acc.y = fmaf(m.x, v.y, acc.y);
+  acc.y = fmaf(m.y, v.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cfma(double2 m, double2 v, double2 acc) {
+  acc.x = fma(m.x, v.x, acc.x);
+  acc.x = fma(-m.y, v.y, acc.x);
+  acc.y = fma(m.x, v.y, acc.y);
+  acc.y = fma(m.y, v.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+template <class C>
+__device__ __forceinline__ C czero();
+template <>
+__device__ __forceinline__ float2 czero<float2>() { return make_float2(0.f, 0.f); }
+template <>
+__device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
+
+__device__ __forceinline__ int insert_zero(int x, int p) { return ((x >> p) << (p + 1)) | (x & ((1 << p) - 1)); }
+
+// ----------------------------------------------------------- op application
+// Dense k-qubit op on one shared-memory tile.  Each compute thread owns whole
+// groups of 2^K amplitudes (the K target bits varied, others fixed); for
+// K <= 2 the matrix lives in registers, otherwise it is read (broadcast) from
+// the shared coefficient pool.
+template <class C, int K>
+__device__ __forceinline__ void tile_dense(C* __restrict__ buf, const OpDesc& op, const C* __restrict__ pool,
+                                           int T, int tid) {
+  constexpr int D = 1 << K;
+  constexpr bool kRegM = K <= 2;
+  C M[kRegM ? D * D : 1];
+  const C* Ms = pool + op.coeff_off;
+  if (kRegM) {
+#pragma unroll
+    for (int e = 0; e < D * D; ++e) M[e] = Ms[e];
+  }
+  int off[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    int o = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b)
+      if ((j >> b) & 1) o |= 1 << op.tgt[b];
+    off[j] = o;
+  }
+  int srt[K];
+#pragma unroll
+  for (int b = 0; b < K; ++b) srt[b] = op.srt[b];
+  const int G = 1 << (T - K);
+  for (int g = tid; g < G; g += kComputeThreads) {
+    int base = g;
+#pragma unroll
+    for (int b = 0; b < K; ++b) base = insert_zero(base, srt[b]);
+    C v[D];
+    if constexpr (K <= 4) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = buf[base + off[j]];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        C acc = czero<C>();
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = cfma(kRegM ? M[i * D + j] : Ms[i * D + j], v[j], acc);
+        buf[base + off[i]] = acc;
+      }
+    } else {  // rare wide CUSTOM gates: keep code size and compile time bounded
+      for (int j = 0; j < D; ++j) v[j] = buf[base + off[j]];
+      for (int i = 0; i < D; ++i) {
+        C acc = czero<C>();
+#pragma unroll 4
+        for (int j = 0; j < D; ++j) acc = cfma(Ms[i * D + j], v[j], acc);
+        buf[base + off[i]] = acc;
+      }
+    }
+  }
+}
+
+// Diagonal op (a merged run of diagonal gates): amp[e] *= table[bits of e at tgt].
+template <class C>
+__device__ __forceinline__ void tile_diag(C* __restrict__ buf, const OpDesc& op, const C* __restrict__ pool,
+                                          int T, int tid) {
+  const C* table = pool + op.coeff_off;
+  const int k = op.k;
+  int tg[kMaxK];
+#pragma unroll
+  for (int b = 0; b < kMaxK; ++b) tg[b] = b < k ? op.tgt[b] : 0;
+  const int N = 1 << T;
+  for (int e = tid; e < N; e += kComputeThreads) {
+    int d = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxK; ++b)
+      if (b < k) d |= ((e >> tg[b]) & 1) << b;
+    buf[e] = cmul(buf[e], table[d]);
+  }
+}
+
+// KMAX bounds the dense arity compiled into a kernel variant, so the common
+// (fused width <= 2) variant carries no register pressure from wide gates.
+template <class C, int KMAX>
+__device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* pool, int T, int tid) {
+  if (op.kind == OP_DIAG) {
+    tile_diag<C>(buf, op, pool, T, tid);
+    return;
+  }
+  switch (op.k) {
+    case 1: tile_dense<C, 1>(buf, op, pool, T, tid); break;
+    case 2: tile_dense<C, 2>(buf, op, pool, T, tid); break;
+    case 3: if constexpr (KMAX >= 3) tile_dense<C, 3>(buf, op, pool, T, tid); break;
+    case 4: if constexpr (KMAX >= 4) tile_dense<C, 4>(buf, op, pool, T, tid); break;
+    case 5: if constexpr (KMAX >= 5) tile_dense<C, 5>(buf, op, pool, T, tid); break;
+    default: if constexpr (KMAX >= 6) tile_dense<C, 6>(buf, op, pool, T, tid); break;
+  }
+}
+
+__device__ __forceinline__ long long tile_base(long long tile, const PassHeader& h) {
+  long long g = tile << h.L;
+  for (int b = 0; b < h.m; ++b) {
+    const int p = h.high[b];
+    g = ((g >> p) << (p + 1)) | (g & ((1LL << p) - 1));
+  }
+  return g;
+}
+__device__ __forceinline__ long long chunk_offset(int c, const PassHeader& h) {
+  long long o = 0;
+  for (int b = 0; b < h.m; ++b)
+    if ((c >> b) & 1) o += 1LL << h.high[b];
+  return o;
+}
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <class C>
+__host__ __device__ inline size_t tile_pass_smem_bytes(const PassHeader& h) {
+  return 128 + align_up(size_t(h.coeff_count) * sizeof(C), 128) + size_t(h.stages) * (sizeof(C) << h.T);
+}
+
+// ------------------------------------------------------------------ kernel
+template <class C, int KMAX>
+__global__ void __launch_bounds__(kThreads, 1) k_tile_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PassHeader& h = args.h;
+  const int S = h.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed   (1 arrival + tx)
+  uint64_t* done = full + S;                            // tile computed (256 arrivals)
+  C* pool = reinterpret_cast<C*>(smem + 128);
+  C* tiles = reinterpret_cast<C*>(smem + 128 + align_up(size_t(h.coeff_count) * sizeof(C), 128));
+  const int tile_elems = 1 << h.T;
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kComputeThreads);
+    }
+    fence_mbar_init();
+  }
+  for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  __syncthreads();
+
+  const long long n_tiles = h.n_tiles;
+  const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (tid >= kComputeThreads) {
+    // ---------------- producer warp: TMA bulk loads / stores
+    const int lane = tid - kComputeThreads;
+    const int n_chunks = 1 << h.m;
+    const uint32_t chunk_bytes = uint32_t(sizeof(C)) << h.L;
+    const uint64_t pol = policy_evict_first();
+    auto tile_of = [&](long long it) { return (long long)blockIdx.x + it * gridDim.x; };
+    auto store_tile = [&](long long it) {
+      const int s = int(it % S);
+      const long long base = tile_base(tile_of(it), h);
+      C* buf = tiles + size_t(s) * tile_elems;
+      for (int c = lane; c < n_chunks; c += 32)
+        bulk_store(amps + base + chunk_offset(c, h), buf + (size_t(c) << h.L), chunk_bytes, pol);
+      bulk_commit();
+    };
+    for (long long it = 0; it < mine; ++it) {
+      const int s = int(it % S);
+      if (it >= S) {
+        mbar_wait(&done[s], uint32_t(((it - S) / S) & 1));
+        store_tile(it - S);
+        bulk_wait_read_all();  // buffer s drained before it is refilled
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
+      __syncwarp();
+      const long long base = tile_base(tile_of(it), h);
+      C* buf = tiles + size_t(s) * tile_elems;
+      for (int c = lane; c < n_chunks; c += 32)
+        bulk_load(buf + (size_t(c) << h.L), amps + base + chunk_offset(c, h), chunk_bytes, &full[s], pol);
+    }
+    for (long long it = (mine > S ? mine - S : 0); it < mine; ++it) {
+      const int s = int(it % S);
+      mbar_wait(&done[s], uint32_t((it / S) & 1));
+      store_tile(it);
+    }
+    bulk_wait_all();
+  } else {
+    // ---------------- compute warps
+    for (long long it = 0; it < mine; ++it) {
+      const int s = int(it % S);
+      mbar_wait(&full[s], uint32_t((it / S) & 1));
+      C* buf = tiles + size_t(s) * tile_elems;
+      for (int o = 0; o < h.n_ops; ++o) {
+        if (o) compute_bar();
+        tile_apply<C, KMAX>(buf, args.ops[o], pool, h.T, tid);
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk store
+      mbar_arrive(&done[s]);
+    }
+  }
+}
+
+// --------------------------------------------------------------- utilities
+template <class C>
+__global__ void k_fill_zero(C* __restrict__ amps, long long n_amps) {
+  // 16-byte stores: 2 c64 or 1 c128 amplitude per word
+  constexpr int per = 16 / sizeof(C);
+  const long long words = n_amps / per;
+  uint4* w = reinterpret_cast<uint4*>(amps);
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x)
+    w[i] = z;
+}
+
+template <class C>
+__global__ void k_set_one(C* amps, long long one) {
+  C v = czero<C>();
+  v.x = 1;
+  amps[one] = v;
+}
+
+template <class C>
+__global__ void k_dot(const C* __restrict__ a, const C* __restrict__ b, long long n, double2* __restrict__ partial) {
+  double re = 0.0, im = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const C x = a[i], y = b[i];
+    const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+    re += xr * yr + xi * yi;  // conj(x) * y
+    im += xr * yi - xi * yr;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  __shared__ double2 red[32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = make_double2(re, im);
+  __syncthreads();
+  if (w == 0) {
+    double2 v = l < (blockDim.x >> 5) ? red[l] : make_double2(0.0, 0.0);
+    for (int o = 16; o > 0; o >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    if (l == 0) partial[blockIdx.x] = v;
+  }
+}
+
+template <class C>
+__global__ void k_probabilities(const C* __restrict__ a, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const C x = a[i];
+    const double r = x.x, m = x.y;
+    out[i] = r * r + m * m;
+  }
+}
+
+}  // namespace svb

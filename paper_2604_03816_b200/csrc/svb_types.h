@@ -1,0 +1,52 @@
+// Shared host/device layout of one tile pass (kernel parameter block).
+//
+// A *pass* streams the whole local state once.  The state is cut into tiles
+// of 2^T amplitudes: tile bits 0..L-1 are the L lowest physical qubits (a
+// contiguous chunk of 2^L amplitudes), tile bits L..L+m-1 are the physical
+// qubits high[0..m-1] (so a tile is 2^m chunks at strides 2^high[b]).  Every
+// kernel op of the pass acts only on tile bits, so one HBM read + write of
+// each amplitude applies all of them.  The whole description travels as a
+// __grid_constant__ kernel parameter (< 32 KB), so a plan needs no device
+// memory and is trivially CUDA-graph capturable.
+#pragma once
+#include <stdint.h>
+
+namespace svb {
+
+constexpr int kMaxOps = 48;        // kernel ops per pass
+constexpr int kMaxHigh = 8;        // high (strided) tile bits
+constexpr int kMaxK = 8;           // targets per kernel op
+constexpr int kMaxDenseK = 6;      // dense ops up to 64x64
+constexpr int kMaxDiagK = 8;       // merged diagonal tables up to 256 entries
+constexpr int kCoeffBytes = 24576; // coefficient pool per pass
+constexpr int kComputeWarps = 8;
+constexpr int kComputeThreads = kComputeWarps * 32;
+constexpr int kThreads = kComputeThreads + 32;   // + one TMA producer warp
+
+enum OpKind : int { OP_DENSE = 0, OP_DIAG = 1 };
+
+struct OpDesc {
+  int kind;           // OpKind
+  int k;              // number of targets
+  int coeff_off;      // element offset into the coefficient pool
+  int pad;
+  int tgt[kMaxK];     // tile-local bit acted on by matrix-local bit j
+  int srt[kMaxK];     // tgt sorted ascending (zero-bit insertion order)
+};
+
+struct PassHeader {
+  int T, L, m, n_ops;
+  int high[kMaxHigh];
+  int coeff_count;    // elements used in the pool
+  int stages;
+  long long n_tiles;
+};
+
+template <class C>
+struct PassArgs {
+  PassHeader h;
+  OpDesc ops[kMaxOps];
+  C coeff[kCoeffBytes / sizeof(C)];
+};
+
+}  // namespace svb

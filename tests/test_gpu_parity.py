@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA engine (through libsvb200.so) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): complex128 max-abs <= 1e-12 and
+fidelity >= 1 - 1e-10; complex64 max-abs <= 1e-5 and fidelity >= 1 - 1e-5,
+fidelity normalised as SURVEY.md 8(a14) explains (the reference's own c64
+norm drift would otherwise consume the budget).  At sizes the oracle cannot
+reach, size-independent properties are used: QFT|0> is exactly uniform,
+mirror circuits C^dagger C return |0>, norms are preserved.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+from golden_io import decode
+from oracle import sv_oracle as orc
+from paper_2604_03816_b200 import generators as gen
+from paper_2604_03816_b200.b200 import B200Engine, plan_options
+from paper_2604_03816_b200.circuit import Circuit, GateKind, GateOp, Precision, effective_unitary
+from paper_2604_03816_b200.engines import AllocationError
+from paper_2604_03816_b200.fusion import fuse
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+TOL = {"double": (1e-12, 1e-10), "single": (1e-5, 1e-5)}
+
+
+@pytest.fixture(scope="module")
+def eng():
+    return B200Engine("b200-test")
+
+
+def assert_close(got: np.ndarray, want: np.ndarray, prec: str, what=""):
+    amax, ftol = TOL[prec]
+    err = float(np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max())
+    fid = orc.normalised_fidelity(got, want)
+    assert err <= amax, f"{what} max-abs {err:.3e} > {amax}"
+    assert fid >= 1 - ftol, f"{what} fidelity 1-{1 - fid:.3e}"
+
+
+def test_known_answers(eng):
+    inv = 1 / math.sqrt(2)
+    s = eng.run_circuit(Circuit(2, [GateOp(GateKind.H, (0,))]))
+    assert np.allclose(s.amplitudes, [inv, inv, 0, 0], atol=1e-15)
+    s = eng.run_circuit(gen.ghz_circuit(2))
+    assert np.allclose(s.amplitudes, [inv, 0, 0, inv], atol=1e-15)
+    for n in (1, 2, 3, 5, 13, 14):
+        for t in range(n):
+            s = eng.run_circuit(Circuit(n, [GateOp(GateKind.X, (t,))]))
+            e = np.zeros(1 << n)
+            e[1 << t] = 1
+            assert np.array_equal(s.amplitudes, e), (n, t)
+    s = eng.run_circuit(gen.ghz_circuit(5))
+    e = np.zeros(32, dtype=complex)
+    e[0] = e[31] = inv
+    assert np.allclose(s.amplitudes, e, atol=1e-15)
+    s = eng.run_circuit(Circuit(3, []))
+    assert np.array_equal(s.amplitudes, [1, 0, 0, 0, 0, 0, 0, 0])
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_golden_random_circuits(eng, golden_random, prec):
+    key = "c128" if prec == "double" else "c64"
+    for i in range(int(golden_random["count"])):
+        c = decode(f"c{i}_", golden_random)
+        want = golden_random[f"c{i}_{key}"]
+        planned = eng.run_circuit(c, Precision(prec))
+        assert planned.amplitudes.dtype == want.dtype
+        assert_close(planned.amplitudes, want, prec, f"plan c{i}")
+        per_gate = eng.run_circuit(c, Precision(prec), checkpoint=lambda s, j: None)
+        assert_close(per_gate.amplitudes, want, prec, f"per-gate c{i}")
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_golden_fused_circuits(eng, golden_fused, prec):
+    key = "c128" if prec == "double" else "c64"
+    for name in golden_fused["names"]:
+        c = decode(f"{name}_fused_", golden_fused)
+        assert_close(eng.run_circuit(c, Precision(prec)).amplitudes,
+                     golden_fused[f"{name}_{key}"], prec, name)
+
+
+OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits": 1, "cost_budget": -1.0},
+        {"no_diag_merge": 1, "stages": 2}, {"stages": 4, "max_ops_per_pass": 1}]
+
+
+@pytest.mark.parametrize("opts", OPTS, ids=[str(o) for o in OPTS])
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_plan_shapes_vs_oracle(prec, opts):
+    e = B200Engine("b200-opts", options=plan_options(**opts) if opts else None)
+    for c in (fuse(gen.layered_circuit(14, layers=6, seed=1), 2)[0],
+              fuse(gen.qft_circuit(13), 2)[0],
+              fuse(gen.layered_circuit(13, layers=4, seed=5), 3)[0],
+              gen.random_su2_circuit(15, 90, seed=3)):
+        want = orc.run_circuit(c, prec)
+        assert_close(e.run_circuit(c, Precision(prec)).amplitudes, want, prec, c.name)
+
+
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_every_target_and_pair(eng, prec):
+    rng = np.random.default_rng(7)
+    n = 15
+    for t in range(n):
+        u = orc.gate_unitary(GateOp(GateKind.U3, (t,), tuple(rng.uniform(0, 6, 3))))
+        c = Circuit(n, [GateOp(GateKind.H, (q,)) for q in range(n)] +
+                    [GateOp(GateKind.CUSTOM, (t,), (), u)])
+        assert_close(eng.run_circuit(c, Precision(prec)).amplitudes, orc.run_circuit(c, prec), prec)
+    for _ in range(12):
+        a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+        z = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+        q, _ = np.linalg.qr(z)
+        c = Circuit(n, [GateOp(GateKind.RY, (x,), (0.3 * x + 0.1,)) for x in range(n)] +
+                    [GateOp(GateKind.CUSTOM, (a, b), (), q)])
+        assert_close(eng.run_circuit(c, Precision(prec)).amplitudes, orc.run_circuit(c, prec), prec)
+
+
+def test_layered20_config1_vs_oracle(eng):
+    """BASELINE config 1 workload (layered-20, c128, fused 693 -> 133)."""
+    f, rep = fuse(gen.layered_circuit(20), 2)
+    assert (rep.original_gate_count, rep.fused_gate_count) == (693, 133)
+    want = orc.run_circuit(f, "double")
+    assert_close(eng.run_circuit(f, Precision.DOUBLE).amplitudes, want, "double", "layered-20")
+    want1 = orc.run_circuit(f, "single")
+    assert_close(eng.run_circuit(f, Precision.SINGLE).amplitudes, want1, "single", "layered-20 c64")
+
+
+def test_qft30_c128_uniform(eng):
+    """BASELINE config 3 at full size: QFT|0...0> is exactly uniform (2^-15)."""
+    import torch
+    f, _ = fuse(gen.qft_circuit(30), 2)
+    s = eng.run_circuit(f, Precision.DOUBLE)
+    dev = s.tensor
+    err = float((dev - (2.0 ** -15)).abs().max().item())
+    assert err <= 1e-12, err
+    assert abs(eng.norm_squared(s) - 1.0) <= 1e-10
+    eng.release(s)
+    del dev
+    torch.cuda.empty_cache()
+
+
+def _dagger(c):
+    return Circuit(c.num_qubits, [GateOp(GateKind.CUSTOM, op.targets, (),
+                                         effective_unitary(op).conj().T) for op in reversed(c.gates)])
+
+
+def test_mirror28_c64(eng):
+    """BASELINE config 2 shape: layered-28 c64, then its inverse -> |0>."""
+    import torch
+    f, _ = fuse(gen.layered_circuit(28), 2)
+    mirror = Circuit(28, list(f.gates) + list(_dagger(f).gates))
+    s = eng.run_circuit(mirror, Precision.SINGLE)
+    a0 = complex(s.tensor[0].item())
+    assert abs(abs(a0) - 1.0) <= 1e-5
+    assert abs(eng.norm_squared(s) - 1.0) <= 1e-5
+    eng.release(s)
+    torch.cuda.empty_cache()
+
+
+def test_reductions(eng):
+    f, _ = fuse(gen.layered_circuit(16, layers=3), 2)
+    a = eng.run_circuit(f, Precision.DOUBLE)
+    b = eng.run_circuit(gen.qft_circuit(16), Precision.DOUBLE)
+    ha, hb = a.amplitudes, b.amplitudes
+    assert abs(eng.inner(a, b) - np.vdot(ha, hb)) <= 1e-12
+    assert abs(eng.norm_squared(a) - np.vdot(ha, ha).real) <= 1e-12
+    assert np.abs(eng.probabilities(a) - np.abs(ha) ** 2).max() <= 1e-15
+    a1 = eng.run_circuit(f, Precision.SINGLE)
+    assert abs(eng.fidelity(a, a1, normalised=True) - 1) <= 1e-6
+
+
+def test_engine_api_contract():
+    e = B200Engine("b200-api", capacity_bytes=16 << 30)
+    with pytest.raises(AllocationError) as ei:
+        e.init_state(30, Precision.DOUBLE)
+    assert ei.value.requested_bytes == 17_179_869_184
+    assert e.live_states == 0
+    s = e.init_state(3, Precision.SINGLE)
+    assert e.live_states == 1
+    assert s.amplitudes.dtype == np.complex64
+    with pytest.raises(ValueError):
+        e.apply_gate(s, GateOp(GateKind.X, (3,)))
+    e.release(s)
+    assert e.live_states == 0
+    with pytest.raises(ValueError):
+        e.init_state(0, Precision.DOUBLE)
+    host = np.zeros(8, dtype=np.complex128)
+    host[5] = 1
+    s = e.adopt(3, Precision.DOUBLE, host)
+    e.apply_gate(s, GateOp(GateKind.X, (0,)))
+    assert s.amplitudes[4] == 1
+    e.release(s)

@@ -1,0 +1,144 @@
+"""CPU checks of the native planner (libsvb200.so, host-only entry points).
+
+1. Legality: executing the input gates in the order the plan applies them
+   (pass by pass) gives the oracle's program-order state.
+2. Lowering: a numpy emulation of what k_tile_pass does with each pass
+   (tile gather by L/high bits, kernel ops on tile-local bits with the
+   planner's merged coefficients, scatter) reproduces the oracle state.
+3. Error behaviour mirrors the reference (ValueError on bad targets).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from golden_io import decode
+from oracle import sv_oracle as orc
+from paper_2604_03816_b200 import generators as gen
+from paper_2604_03816_b200.b200 import CircuitPlan, plan_options
+from paper_2604_03816_b200.circuit import Circuit, GateKind, GateOp, Precision
+from paper_2604_03816_b200.fusion import fuse
+
+
+def tile_indices(n: int, info: dict, tile: int) -> np.ndarray:
+    """Global amplitude index of every tile-local index (the kernel's addressing)."""
+    L, high, T = info["low_bits"], info["high"], info["tile_bits"]
+    g = tile << L
+    for p in high:
+        g = ((g >> p) << (p + 1)) | (g & ((1 << p) - 1))
+    local = np.arange(1 << T)
+    idx = np.full(1 << T, g, dtype=np.int64) + (local & ((1 << L) - 1))
+    for b, p in enumerate(high):
+        idx += ((local >> (L + b)) & 1) << p
+    return idx
+
+
+def emulate(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
+    amps = orc.init_state(n, precision)
+    nat = plan.native
+    for p in range(nat.num_passes()):
+        info = nat.pass_info(p)
+        T = info["tile_bits"]
+        ops = [nat.kernel_op(p, i) for i in range(info["num_kernel_ops"])]
+        for tile in range(1 << (n - T)):
+            idx = tile_indices(n, info, tile)
+            buf = amps[idx].copy()
+            for op in ops:
+                if op["kind"] == "dense":
+                    u = op["coeffs"].reshape(1 << op["k"], 1 << op["k"])
+                    orc.apply_matrix(buf, T, op["targets"], u)
+                else:
+                    d = np.zeros(1 << T, dtype=np.int64)
+                    e = np.arange(1 << T)
+                    for b, t in enumerate(op["targets"]):
+                        d |= ((e >> t) & 1) << b
+                    buf *= op["coeffs"].astype(buf.dtype)[d]
+            amps[idx] = buf
+    return amps
+
+
+def plan_order_state(plan: CircuitPlan, circuit, precision: str) -> np.ndarray:
+    amps = orc.init_state(circuit.num_qubits, precision)
+    seen = []
+    for p in range(plan.native.num_passes()):
+        for gi in plan.native.pass_gates(p):
+            orc.apply_gate(amps, circuit.num_qubits, circuit.gates[gi])
+            seen.append(gi)
+    assert sorted(seen) == list(range(len(circuit.gates)))
+    return amps
+
+
+CASES = [
+    ("layered8", lambda: fuse(gen.layered_circuit(8, layers=6), 2)[0]),
+    ("layered9_w3", lambda: fuse(gen.layered_circuit(9, layers=5, seed=2), 3)[0]),
+    ("qft9", lambda: fuse(gen.qft_circuit(9), 2)[0]),
+    ("qft8_raw", lambda: gen.qft_circuit(8)),
+    ("su2", lambda: gen.random_su2_circuit(7, 60, seed=4)),
+]
+OPTIONS = [
+    {},
+    {"tile_bits": 5, "min_low_bits": 2},
+    {"tile_bits": 4, "min_low_bits": 1, "cost_budget": -1.0},
+    {"tile_bits": 6, "min_low_bits": 3, "no_diag_merge": 1},
+    {"tile_bits": 5, "min_low_bits": 1, "max_ops_per_pass": 2},
+]
+
+
+@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("opts", OPTIONS, ids=[str(o) for o in OPTIONS])
+def test_plan_legal_and_lowering(name, make, opts):
+    c = make()
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates, plan_options(**opts) if opts else None)
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+    assert np.abs(emulate(plan, c.num_qubits, "double") - want).max() <= 1e-12
+    # single precision plans round coefficients like ref engines.py:157
+    plan1 = CircuitPlan(c.num_qubits, Precision.SINGLE, c.gates, plan_options(**opts) if opts else None)
+    got = emulate(plan1, c.num_qubits, "single")
+    assert np.abs(got - want).max() <= 1e-5
+
+
+def test_plan_golden_random_circuits(golden_random):
+    for i in range(int(golden_random["count"])):
+        c = decode(f"c{i}_", golden_random)
+        plan = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates,
+                           plan_options(tile_bits=min(4, c.num_qubits), min_low_bits=1))
+        got = emulate(plan, c.num_qubits, "double")
+        assert np.abs(got - golden_random[f"c{i}_c128"]).max() <= 1e-12, i
+
+
+def test_plan_structure_layered28():
+    f, _ = fuse(gen.layered_circuit(28), 2)
+    for prec in (Precision.SINGLE, Precision.DOUBLE):
+        plan = CircuitPlan(28, prec, f.gates)
+        passes = plan.passes()
+        assert sum(p["num_gates"] for p in passes) == len(f.gates) == 189
+        assert len(passes) < len(f.gates) / 3
+        for p in passes:
+            assert p["low_bits"] + len(p["high"]) == p["tile_bits"]
+            assert p["low_bits"] >= (6 if prec is Precision.SINGLE else 5)
+
+
+def test_diagonal_runs_are_merged_qft():
+    f, _ = fuse(gen.qft_circuit(20), 2)
+    plan = CircuitPlan(20, Precision.DOUBLE, f.gates)
+    n_ops = sum(p["num_kernel_ops"] for p in plan.passes())
+    assert n_ops < len(f.gates) / 2
+
+
+def test_planner_errors():
+    with pytest.raises(ValueError):
+        CircuitPlan(3, Precision.DOUBLE, [GateOp(GateKind.X, (3,))])
+    with pytest.raises(ValueError):
+        CircuitPlan(0, Precision.DOUBLE, [])
+    wide = GateOp(GateKind.CUSTOM, tuple(range(7)), (), np.eye(128))
+    with pytest.raises(ValueError):
+        CircuitPlan(8, Precision.DOUBLE, [wide])
+
+
+def test_empty_and_single_qubit_states():
+    plan = CircuitPlan(1, Precision.SINGLE, [GateOp(GateKind.H, (0,))])
+    assert plan.num_passes == 1
+    got = emulate(plan, 1, "single")
+    assert np.allclose(got, [2 ** -0.5, 2 ** -0.5], atol=1e-7)
+    assert CircuitPlan(3, Precision.DOUBLE, []).num_passes == 0
