@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--tile-bits", type=int, default=0)
     ap.add_argument("--min-low-bits", type=int, default=0)
+    ap.add_argument("--reg-bits", type=int, default=0)
+    ap.add_argument("--no-reg-phases", action="store_true")
     return ap.parse_args()
 
 
@@ -228,7 +230,8 @@ def run_b200(args):
     from paper_2604_03816_b200.circuit import Precision
     precision = Precision(prec)
     opts = plan_options(cost_budget=args.cost_budget, stages=args.stages,
-                        tile_bits=args.tile_bits, min_low_bits=args.min_low_bits)
+                        tile_bits=args.tile_bits, min_low_bits=args.min_low_bits,
+                        reg_bits=args.reg_bits, no_reg_phases=int(args.no_reg_phases))
     eng = B200Engine("b200-bench", device=local, options=opts)
 
     if world > 1:

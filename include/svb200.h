@@ -56,6 +56,8 @@ typedef struct svb_plan_options {
                            time; 0: default 1.0, <0: unlimited                       */
   int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
   int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
+  int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 4 for c64, 3 c128) */
+  int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */
@@ -67,6 +69,8 @@ typedef struct svb_pass_info {
   int num_kernel_ops;   /* ops the kernel applies (after diagonal merging) */
   int num_gates;        /* input gates covered by this pass */
   double est_cost;      /* planner cost estimate (fraction of HBM time) */
+  int reg_bits;         /* > 0: register-phase kernel with 2^reg_bits amps per thread */
+  int num_phases;       /* register phases (0 for the shared-memory kernel) */
 } svb_pass_info;
 
 int svb_abi_version(void);
@@ -100,6 +104,12 @@ int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap);
  * coefficients as complex128 (dense 4^k, diagonal 2^k entries). */
 int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* tile_targets,
                        double* coeffs, int coeff_cap);
+/* Register phase `phase` of pass `pass`: R[4] register bits, op range, flags. */
+int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_begin, int* op_end,
+                   int* flags);
+/* Register-phase encoding of kernel op i: dense -> *mask, diagonal -> src[k]. */
+int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
+                      double* coeffs, int coeff_cap);
 int svb_plan_execute(svb_plan* plan, void* amps, void* stream);
 int svb_plan_execute_range(svb_plan* plan, void* amps, int first_pass, int num_passes, void* stream);
 void svb_plan_destroy(svb_plan* plan);

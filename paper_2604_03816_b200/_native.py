@@ -22,7 +22,8 @@ ABI_VERSION = 1
 EXPORTS = (
     "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
     "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
-    "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_execute",
+    "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
+    "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
     "svb_probabilities",
 )
@@ -31,13 +32,14 @@ EXPORTS = (
 class PlanOptions(C.Structure):
     _fields_ = [("tile_bits", C.c_int), ("min_low_bits", C.c_int),
                 ("max_ops_per_pass", C.c_int), ("cost_budget", C.c_double),
-                ("no_diag_merge", C.c_int), ("stages", C.c_int)]
+                ("no_diag_merge", C.c_int), ("stages", C.c_int), ("reg_bits", C.c_int),
+                ("no_reg_phases", C.c_int)]
 
 
 class PassInfo(C.Structure):
     _fields_ = [("tile_bits", C.c_int), ("low_bits", C.c_int), ("num_high", C.c_int),
                 ("high", C.c_int * 8), ("num_kernel_ops", C.c_int), ("num_gates", C.c_int),
-                ("est_cost", C.c_double)]
+                ("est_cost", C.c_double), ("reg_bits", C.c_int), ("num_phases", C.c_int)]
 
 
 class NativeError(RuntimeError):
@@ -72,6 +74,8 @@ def lib():
         "svb_plan_pass_info": (i, [vp, i, C.POINTER(PassInfo)]),
         "svb_plan_pass_gates": (i, [vp, i, ip, i]),
         "svb_plan_kernel_op": (i, [vp, i, i, ip, ip, ip, dp, i]),
+        "svb_plan_phase": (i, [vp, i, i, ip, ip, ip, ip]),
+        "svb_plan_phase_op": (i, [vp, i, i, ip, ip, ip, ip, dp, i]),
         "svb_plan_execute": (i, [vp, vp, vp]),
         "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
         "svb_plan_destroy": (None, [vp]),
@@ -137,7 +141,22 @@ class NativePlan:
         return {"tile_bits": info.tile_bits, "low_bits": info.low_bits,
                 "high": [info.high[b] for b in range(info.num_high)],
                 "num_kernel_ops": info.num_kernel_ops, "num_gates": info.num_gates,
-                "est_cost": info.est_cost}
+                "est_cost": info.est_cost, "reg_bits": info.reg_bits, "num_phases": info.num_phases}
+
+    def phase(self, p: int, f: int) -> dict:
+        R = (C.c_int * 4)()
+        b, e, fl = C.c_int(), C.c_int(), C.c_int()
+        check(lib().svb_plan_phase(self._h, p, f, R, C.byref(b), C.byref(e), C.byref(fl)))
+        return {"R": list(R), "op_begin": b.value, "op_end": e.value, "flags": fl.value}
+
+    def phase_op(self, p: int, i: int) -> dict:
+        kind, k, mask = C.c_int(), C.c_int(), C.c_int()
+        src = np.zeros(SVB_MAX_TARGETS, dtype=np.int32)
+        co = np.zeros(2 * 4096, dtype=np.float64)
+        n = check(lib().svb_plan_phase_op(self._h, p, i, C.byref(kind), C.byref(k), C.byref(mask),
+                                          _iptr(src), _dptr(co), 4096))
+        return {"kind": "diag" if kind.value == 1 else "dense", "k": k.value, "mask": mask.value,
+                "src": [int(x) for x in src[:k.value]], "coeffs": co[:2 * n].view(np.complex128).copy()}
 
     def pass_gates(self, p: int) -> list[int]:
         buf = np.zeros(max(1, self.num_gates), dtype=np.int32)

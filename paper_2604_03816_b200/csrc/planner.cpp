@@ -10,6 +10,7 @@ namespace svb {
 
 int default_tile_bits(int prec) { return prec == SVB_C64 ? 12 : 11; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
+int default_reg_bits(int prec) { return prec == SVB_C64 ? 4 : 3; }
 
 namespace {
 
@@ -25,15 +26,16 @@ struct CostModel {
     fma = prec == SVB_C64 ? 128.0 : 64.0;
     mem = 2.0 * s / 23.0;
   }
+  // register-resident ops: FMAs plus, amortised, half a shared-memory
+  // transpose per dense op (phases hold ~2 dense ops)
   double dense(int k) const {
     double flops = 4.0 * double(1 << k) / fma;
-    double smem = 2.0 * s / 128.0 + (k >= 3 ? double(1 << k) * s / 128.0 / 8.0 : 0.0);
-    return (std::max(flops, smem) * 1.15 + 0.02) / mem;
+    double smem = 0.5 * 2.0 * s / 128.0;
+    return (flops * 1.2 + smem) / mem;
   }
   double diag(int k) const {
-    double flops = 4.0 / fma + 2.0 * k / 64.0;
-    double smem = 3.0 * s / 128.0;
-    return (std::max(flops, smem) * 1.15 + 0.02) / mem;
+    double flops = 4.0 / fma + (1.0 + k) / 64.0;
+    return (flops * 1.2 + s / 128.0) / mem;
   }
   double of(const Gate& g) const { return g.diag ? diag(g.k) : dense(g.k); }
 };
@@ -104,6 +106,103 @@ struct DiagAcc {
 };
 
 size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
+
+// Partition a lowered pass into register phases (k_reg_pass).  Dense ops are
+// kept in program order; a new phase starts when the union of register bits
+// would exceed RB.  Diagonal ops ride in whatever phase is current.  Returns
+// false when the pass must use the shared-memory kernel instead.
+bool build_phases(Pass& p, int RB, int prec) {
+  if (RB < 1 || RB > 4 || p.T != RB + 8) return false;
+  for (const KernelOp& op : p.ops)
+    if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
+  std::vector<std::vector<int>> sets;
+  std::vector<std::pair<int, int>> ranges;
+  std::vector<int> cur;
+  int begin = 0;
+  for (int i = 0; i < int(p.ops.size()); ++i) {
+    const KernelOp& op = p.ops[i];
+    if (op.kind == OP_DIAG) continue;
+    std::vector<int> u = cur;
+    for (int j = 0; j < op.k; ++j)
+      if (std::find(u.begin(), u.end(), op.tgt[j]) == u.end()) u.push_back(op.tgt[j]);
+    if (int(u.size()) <= RB) {
+      cur.swap(u);
+    } else {
+      sets.push_back(cur);
+      ranges.emplace_back(begin, i);
+      begin = i;
+      cur.assign(op.tgt, op.tgt + op.k);
+    }
+  }
+  sets.push_back(cur);
+  ranges.emplace_back(begin, int(p.ops.size()));
+  if (int(sets.size()) > kMaxPhases) return false;
+  const int low_conflict = prec == SVB_C64 ? 4 : 3;  // bank-row index bits
+  p.phases.clear();
+  p.reg_ops.assign(p.ops.size(), RegOp());
+  for (size_t ph = 0; ph < sets.size(); ++ph) {
+    std::vector<int> R = sets[ph];
+    for (int b = p.T - 1; b >= 0 && int(R.size()) < RB; --b)  // fill with high tile bits
+      if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
+    std::sort(R.begin(), R.end());
+    RegPhase rp;
+    for (int i = 0; i < RB; ++i) rp.R[i] = R[i];
+    rp.op_begin = ranges[ph].first;
+    rp.op_end = ranges[ph].second;
+    const bool low = R[0] < low_conflict;
+    if (ph == 0 && low) rp.flags |= PH_TRANSPOSE_IN;
+    if (ph + 1 == sets.size() && low) rp.flags |= PH_TRANSPOSE_OUT;
+    auto reg_of = [&](int t) {
+      for (int i = 0; i < RB; ++i)
+        if (R[i] == t) return i;
+      return -1;
+    };
+    auto thread_bit_of = [&](int t) {
+      int k = 0;
+      for (int q = 0; q < t; ++q)
+        if (std::find(R.begin(), R.end(), q) == R.end()) ++k;
+      return k;
+    };
+    for (int i = rp.op_begin; i < rp.op_end; ++i) {
+      const KernelOp& op = p.ops[i];
+      RegOp& ro = p.reg_ops[i];
+      ro.kind = op.kind;
+      ro.k = op.k;
+      if (op.kind == OP_DIAG) {
+        for (int b = 0; b < op.k; ++b) {
+          const int r = reg_of(op.tgt[b]);
+          ro.src[b] = r >= 0 ? r : 16 + thread_bit_of(op.tgt[b]);
+        }
+        ro.coeff = op.coeff;
+      } else {
+        int ri[kMaxK];
+        for (int j = 0; j < op.k; ++j) {
+          ri[j] = reg_of(op.tgt[j]);
+          if (ri[j] < 0) return false;  // cannot happen by construction
+          ro.mask |= 1 << ri[j];
+        }
+        // new local bit j' <-> j'-th lowest register bit; pos[j] = rank of ri[j]
+        int pos[kMaxK];
+        for (int j = 0; j < op.k; ++j) {
+          pos[j] = 0;
+          for (int j2 = 0; j2 < op.k; ++j2) pos[j] += ri[j2] < ri[j];
+        }
+        const int D = 1 << op.k;
+        auto old_index = [&](int a) {
+          int o = 0;
+          for (int j = 0; j < op.k; ++j) o |= ((a >> pos[j]) & 1) << j;
+          return o;
+        };
+        ro.coeff.assign(size_t(D) * D, cd());
+        for (int a = 0; a < D; ++a)
+          for (int b = 0; b < D; ++b) ro.coeff[size_t(a) * D + b] = op.coeff[size_t(old_index(a)) * D + old_index(b)];
+      }
+    }
+    p.phases.push_back(rp);
+  }
+  p.reg_bits = RB;
+  return true;
+}
 
 }  // namespace
 
@@ -342,6 +441,12 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     }
     p.ops = std::move(ops);
     p.num_gates = int(taken.size());
+    const int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
+    if (!opt.no_reg_phases && !build_phases(p, RB, prec)) {
+      p.phases.clear();
+      p.reg_ops.clear();
+      p.reg_bits = 0;
+    }
     p.cost = 0.0;
     for (auto& o : p.ops) p.cost += o.kind == OP_DIAG ? cm.diag(o.k) : cm.dense(o.k);
     plan.passes.push_back(std::move(p));

@@ -34,12 +34,29 @@ struct KernelOp {
   std::vector<int> gates;  // input gates folded into this op, program order
 };
 
+// Register-phase encoding of a pass for k_reg_pass (see svb_regpass.cuh).
+struct RegPhase {
+  int R[4] = {0, 0, 0, 0};  // register bit i <-> tile-local bit R[i] (ascending)
+  int op_begin = 0, op_end = 0;
+  int flags = 0;
+};
+struct RegOp {
+  int kind = OP_DENSE;
+  int k = 0;
+  int mask = 0;            // dense: register-bit mask
+  int src[kMaxK] = {0};    // diagonal: register index, or 16 + thread-bit index
+  std::vector<cd> coeff;   // dense: matrix permuted to ascending register bits
+};
+
 struct Pass {
   int T = 0, L = 0, m = 0;
   int high[kMaxHigh] = {0};
   std::vector<KernelOp> ops;
   double cost = 0.0;
   int num_gates = 0;
+  int reg_bits = 0;               // > 0: executed by k_reg_pass<RB = reg_bits>
+  std::vector<RegPhase> phases;
+  std::vector<RegOp> reg_ops;     // same order as ops
 };
 
 struct Plan {
@@ -52,6 +69,7 @@ struct Plan {
 // Tile defaults per precision: 32 KiB tiles, 512-byte contiguous chunks.
 int default_tile_bits(int prec);
 int default_min_low_bits(int prec);
+int default_reg_bits(int prec);
 
 // Parse + classify the raw ABI arrays into gates (diagonal detection).
 bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const double* op_mats,

@@ -17,6 +17,7 @@
 #include "planner.h"
 #include "svb200.h"
 #include "svb_kernels.cuh"
+#include "svb_regpass.cuh"
 
 using namespace svb;
 
@@ -58,9 +59,11 @@ int device_facts(DeviceFacts** out) {
     SVB_CUDA(cudaDeviceGetAttribute(&f.sm_count, cudaDevAttrMultiProcessorCount, dev));
     int max_optin = 0;
     SVB_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const void* fns[] = {(const void*)k_tile_pass<float2, 2>, (const void*)k_tile_pass<float2, 3>,
-                         (const void*)k_tile_pass<float2, 6>, (const void*)k_tile_pass<double2, 2>,
-                         (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>};
+    const void* fns[] = {(const void*)k_tile_pass<float2, 2>,  (const void*)k_tile_pass<float2, 3>,
+                         (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
+                         (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
+                         (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
+                         (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
     f.attrs_set = true;
@@ -78,7 +81,36 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
   a.h.n_ops = int(p.ops.size());
   for (int b = 0; b < p.m; ++b) a.h.high[b] = p.high[b];
   a.h.stages = stages;
+  a.h.n_phases = int(p.phases.size());
+  a.h.reg_bits = p.reg_bits;
   int off = 0;
+  if (!p.phases.empty()) {
+    for (size_t f = 0; f < p.phases.size(); ++f) {
+      PhaseDesc& d = a.phases[f];
+      std::memset(&d, 0, sizeof(d));
+      d.op_begin = p.phases[f].op_begin;
+      d.op_end = p.phases[f].op_end;
+      d.flags = p.phases[f].flags;
+      for (int i = 0; i < 4; ++i) d.R[i] = p.phases[f].R[i];
+    }
+    for (size_t i = 0; i < p.reg_ops.size(); ++i) {
+      const RegOp& ro = p.reg_ops[i];
+      OpDesc& d = a.ops[i];
+      std::memset(&d, 0, sizeof(d));
+      d.kind = ro.kind;
+      d.k = ro.k;
+      d.coeff_off = off;
+      d.pad = ro.mask;
+      for (int j = 0; j < ro.k; ++j) d.tgt[j] = ro.src[j];
+      for (const cd& z : ro.coeff) {
+        a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
+        a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
+        ++off;
+      }
+    }
+    a.h.coeff_count = off;
+    return;
+  }
   for (size_t i = 0; i < p.ops.size(); ++i) {
     const KernelOp& ko = p.ops[i];
     OpDesc& d = a.ops[i];
@@ -115,10 +147,16 @@ int launch_pass(const PassArgs<C>& a0, int n_local, C* amps, cudaStream_t stream
   if (rc) return rc;
   const PassArgs<C>& a = a0;
   const size_t smem = tile_pass_smem_bytes<C>(a.h);
-  int kmax = 0;
-  for (int i = 0; i < a.h.n_ops; ++i)
-    if (a.ops[i].kind == OP_DENSE) kmax = std::max(kmax, a.ops[i].k);
-  void (*fn)(C*, PassArgs<C>) = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
+  void (*fn)(C*, PassArgs<C>);
+  if (a.h.n_phases > 0) {
+    fn = a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
+    if (a.h.reg_bits != 3 && a.h.reg_bits != 4) return fail(SVB_EUNSUPPORTED, "reg_bits must be 3 or 4");
+  } else {
+    int kmax = 0;
+    for (int i = 0; i < a.h.n_ops; ++i)
+      if (a.ops[i].kind == OP_DENSE) kmax = std::max(kmax, a.ops[i].k);
+    fn = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
+  }
   int per_sm = 0;
   SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
   if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tile pass does not fit on an SM (shared memory)");
@@ -262,7 +300,43 @@ int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out) {
   out->num_kernel_ops = int(p.ops.size());
   out->num_gates = p.num_gates;
   out->est_cost = p.cost;
+  out->reg_bits = p.reg_bits;
+  out->num_phases = int(p.phases.size());
   return SVB_OK;
+}
+
+int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_begin, int* op_end, int* flags) {
+  if (!plan || !R || !op_begin || !op_end || !flags) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (phase < 0 || phase >= int(p.phases.size())) return fail(SVB_EINVAL, "phase index out of range");
+  const RegPhase& ph = p.phases[phase];
+  for (int i = 0; i < 4; ++i) R[i] = ph.R[i];
+  *op_begin = ph.op_begin;
+  *op_end = ph.op_end;
+  *flags = ph.flags;
+  return SVB_OK;
+}
+
+int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
+                      double* coeffs, int coeff_cap) {
+  if (!plan || !kind || !k || !mask || !src) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (i < 0 || i >= int(p.reg_ops.size())) return fail(SVB_EINVAL, "op index out of range");
+  const RegOp& op = p.reg_ops[i];
+  *kind = op.kind;
+  *k = op.k;
+  *mask = op.mask;
+  for (int j = 0; j < op.k; ++j) src[j] = op.src[j];
+  if (coeffs) {
+    if (int(op.coeff.size()) > coeff_cap) return fail(SVB_EINVAL, "coefficient capacity too small");
+    for (size_t e = 0; e < op.coeff.size(); ++e) {
+      coeffs[2 * e] = op.coeff[e].real();
+      coeffs[2 * e + 1] = op.coeff[e].imag();
+    }
+  }
+  return int(op.coeff.size());
 }
 
 int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap) {

@@ -1,0 +1,300 @@
+// k_reg_pass -- register-resident tile pass (the production path for tiles of
+// T = RB + 8 qubits).
+//
+// Each of the 256 compute threads holds 2^RB amplitudes of the tile in
+// registers.  A pass is a sequence of *phases*; phase p fixes which RB tile
+// bits are register bits (R_p) -- the other 8 tile bits are the thread index.
+// Every dense op of the phase targets only register bits and runs as fully
+// unrolled FMAs on registers (no address math, no shared-memory traffic);
+// diagonal ops run on any bits.  Between phases the tile is transposed
+// through shared memory in an XOR-swizzled layout (conflict-free for almost
+// every R).  Data arrive by 1-D TMA bulk copies (producer warp, ring of
+// `stages` buffers); the last phase writes its registers straight to HBM
+// (coalesced when the register bits avoid the 3-4 lowest qubits), so a buffer
+// is released to the producer as soon as the last phase has read it.
+#pragma once
+#include "svb_kernels.cuh"
+
+namespace svb {
+
+template <class C>
+struct Swz;
+template <>
+struct Swz<float2> {  // 16 x 8 B per 128-B bank row
+  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 4) ^ (i >> 8)) & 15); }
+};
+template <>
+struct Swz<double2> {  // 8 x 16 B per 128-B bank row
+  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7); }
+};
+
+template <int RB>
+__host__ __device__ constexpr int deposit_mask(int x, int mask) {
+  int r = 0, b = 0;
+  for (int i = 0; i < RB; ++i)
+    if ((mask >> i) & 1) {
+      if ((x >> b) & 1) r |= 1 << i;
+      ++b;
+    }
+  return r;
+}
+__host__ __device__ constexpr int popc_c(int m) { return m ? (m & 1) + popc_c(m >> 1) : 0; }
+
+// Dense op on register bits MASK (matrix-local bit j <-> j-th lowest set bit).
+template <class C, int RB, int MASK>
+__device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__ Ms) {
+  constexpr int K = popc_c(MASK);
+  constexpr int D = 1 << K;
+  constexpr int REST = ((1 << RB) - 1) & ~MASK;
+  C M[D * D];
+#pragma unroll
+  for (int e = 0; e < D * D; ++e) M[e] = Ms[e];
+#pragma unroll
+  for (int g = 0; g < (1 << (RB - K)); ++g) {
+    const int base = deposit_mask<RB>(g, REST);
+    C in[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) in[j] = v[base | deposit_mask<RB>(j, MASK)];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      C acc = czero<C>();
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc = cfma(M[i * D + j], in[j], acc);
+      v[base | deposit_mask<RB>(i, MASK)] = acc;
+    }
+  }
+}
+
+// Diagonal op: table index bit b comes from register bit (src<16) or thread bit (src-16).
+template <class C, int RB>
+__device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, const C* __restrict__ table, int tid) {
+  int dt = 0;
+  int contrib[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) contrib[i] = 0;
+  for (int b = 0; b < op.k; ++b) {
+    const int src = op.tgt[b];
+    if (src >= 16)
+      dt |= ((tid >> (src - 16)) & 1) << b;
+    else {
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        if (i == src) contrib[i] = 1 << b;
+    }
+  }
+#pragma unroll
+  for (int rho = 0; rho < (1 << RB); ++rho) {
+    int d = dt;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if ((rho >> i) & 1) d |= contrib[i];
+    v[rho] = cmul(v[rho], table[d]);
+  }
+}
+
+template <class C, int RB>
+__device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, const C* pool, int tid) {
+  const C* co = pool + op.coeff_off;
+  if (op.kind == OP_DIAG) {
+    reg_diag<C, RB>(v, op, co, tid);
+    return;
+  }
+  switch (op.pad) {  // register-bit mask of the dense op
+#define SVB_CASE(m) \
+  case m:           \
+    if constexpr ((m) < (1 << RB) && popc_c(m) <= 3) reg_dense<C, RB, (m)>(v, co); \
+    break;
+    SVB_CASE(1) SVB_CASE(2) SVB_CASE(3) SVB_CASE(4) SVB_CASE(5) SVB_CASE(6) SVB_CASE(7)
+    SVB_CASE(8) SVB_CASE(9) SVB_CASE(10) SVB_CASE(11) SVB_CASE(12) SVB_CASE(13) SVB_CASE(14)
+#undef SVB_CASE
+    default: break;
+  }
+}
+
+// Per-thread addressing of one phase: tile-local index of register rho is
+// base | sum_i bit_i(rho) << R[i]; thread bits are deposited at the non-R bits.
+template <int RB>
+struct PhaseAddr {
+  int base;
+  int offr[RB];
+  __device__ __forceinline__ PhaseAddr(const PhaseDesc& ph, int T, int tid) {
+    int used = 0;
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      offr[i] = 1 << ph.R[i];
+      used |= offr[i];
+    }
+    base = 0;
+    int k = 0;
+    for (int p = 0; p < T; ++p)
+      if (!((used >> p) & 1)) {
+        base |= ((tid >> k) & 1) << p;
+        ++k;
+      }
+  }
+  __device__ __forceinline__ int idx(int rho) const {
+    int x = base;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if ((rho >> i) & 1) x += offr[i];
+    return x;
+  }
+};
+
+// Tile-local bit p -> global (shard) bit: low bits map to themselves, bit L+b
+// to high[b].  Global offset of a tile-local index = tile_base + gthr + sum of
+// the register offsets selected by rho (<= RB 64-bit adds per amplitude).
+__device__ __forceinline__ int gpos(int p, const PassHeader& h) { return p < h.L ? p : h.high[p - h.L]; }
+
+template <int RB>
+struct GlobalAddr {
+  long long gthr;
+  long long goff[RB];
+  __device__ __forceinline__ long long at(int rho) const {
+    long long x = gthr;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if ((rho >> i) & 1) x += goff[i];
+    return x;
+  }
+};
+
+// layout of phase `ph` (thread bits at the non-R tile bits)
+template <int RB>
+__device__ __forceinline__ GlobalAddr<RB> phase_gaddr(const PhaseDesc& ph, const PassHeader& h, int T, int tid) {
+  GlobalAddr<RB> g;
+  int used = 0;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    g.goff[i] = 1LL << gpos(ph.R[i], h);
+    used |= 1 << ph.R[i];
+  }
+  g.gthr = 0;
+  int k = 0;
+  for (int p = 0; p < T; ++p)
+    if (!((used >> p) & 1)) {
+      if ((tid >> k) & 1) g.gthr += 1LL << gpos(p, h);
+      ++k;
+    }
+  return g;
+}
+
+// linear layout x = rho * 256 + tid (bits 0..7 from tid, 8.. from rho)
+template <int RB>
+__device__ __forceinline__ GlobalAddr<RB> linear_gaddr(const PassHeader& h, int tid) {
+  GlobalAddr<RB> g;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) g.goff[i] = 1LL << gpos(8 + i, h);
+  g.gthr = 0;
+  for (int p = 0; p < 8; ++p)
+    if ((tid >> p) & 1) g.gthr += 1LL << gpos(p, h);
+  return g;
+}
+
+template <class C, int RB>
+__global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+  constexpr int T = RB + 8;
+  constexpr int NR = 1 << RB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const PassHeader& h = args.h;
+  const int S = h.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed (1 arrival + tx bytes)
+  uint64_t* empty = full + S;                           // tile buffer drained (256 arrivals)
+  C* pool = reinterpret_cast<C*>(smem + 128);
+  C* tiles = reinterpret_cast<C*>(smem + 128 + align_up(size_t(h.coeff_count) * sizeof(C), 128));
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kComputeThreads);
+    }
+    fence_mbar_init();
+  }
+  for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  __syncthreads();
+
+  const long long n_tiles = h.n_tiles;
+  const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (tid >= kComputeThreads) {
+    // ------------------------------------------------ producer: TMA loads only
+    const int lane = tid - kComputeThreads;
+    const int n_chunks = 1 << h.m;
+    const uint32_t chunk_bytes = uint32_t(sizeof(C)) << h.L;
+    const uint64_t pol = policy_evict_first();
+    for (long long it = 0; it < mine; ++it) {
+      const int s = int(it % S);
+      if (it >= S) mbar_wait(&empty[s], uint32_t(((it - S) / S) & 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
+      __syncwarp();
+      const long long base = tile_base((long long)blockIdx.x + it * gridDim.x, h);
+      C* buf = tiles + (size_t(s) << T);
+      for (int c = lane; c < n_chunks; c += 32)
+        bulk_load(buf + (size_t(c) << h.L), amps + base + chunk_offset(c, h), chunk_bytes, &full[s], pol);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------- compute threads
+  const int np = h.n_phases;
+  for (long long it = 0; it < mine; ++it) {
+    const int s = int(it % S);
+    const long long tile = (long long)blockIdx.x + it * gridDim.x;
+    C* buf = tiles + (size_t(s) << T);
+    mbar_wait(&full[s], uint32_t((it / S) & 1));
+    C v[NR];
+    for (int p = 0; p < np; ++p) {
+      const PhaseDesc& ph = args.phases[p];
+      const PhaseAddr<RB> a(ph, T, tid);
+      if (p == 0) {
+        if (ph.flags & PH_TRANSPOSE_IN) {
+          // linear (TMA) layout -> swizzled layout, contiguous conflict-free reads
+#pragma unroll
+          for (int r = 0; r < NR; ++r) v[r] = buf[r * kComputeThreads + tid];
+          compute_bar();
+#pragma unroll
+          for (int r = 0; r < NR; ++r) buf[Swz<C>::f(r * kComputeThreads + tid)] = v[r];
+          compute_bar();
+#pragma unroll
+          for (int r = 0; r < NR; ++r) v[r] = buf[Swz<C>::f(a.idx(r))];
+        } else {
+#pragma unroll
+          for (int r = 0; r < NR; ++r) v[r] = buf[a.idx(r)];
+          // all reads of the linear layout must finish before swizzled writes
+          if (np > 1 || (ph.flags & PH_TRANSPOSE_OUT)) compute_bar();
+        }
+      } else {
+        compute_bar();
+#pragma unroll
+        for (int r = 0; r < NR; ++r) v[r] = buf[Swz<C>::f(a.idx(r))];
+      }
+      const bool last = p == np - 1;
+      if (last && !(ph.flags & PH_TRANSPOSE_OUT)) mbar_arrive(&empty[s]);  // buffer free for the next load
+      for (int o = ph.op_begin; o < ph.op_end; ++o) reg_apply<C, RB>(v, args.ops[o], pool, tid);
+      if (!last) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) buf[Swz<C>::f(a.idx(r))] = v[r];
+      } else if (!(ph.flags & PH_TRANSPOSE_OUT)) {
+        // direct store from registers (coalesced when R avoids the lowest bits)
+        const GlobalAddr<RB> ga = phase_gaddr<RB>(ph, h, T, tid);
+        C* __restrict__ dst = amps + tile_base(tile, h);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) dst[ga.at(r)] = v[r];
+      } else {
+        // swizzled smem, then contiguous reads -> coalesced global stores
+#pragma unroll
+        for (int r = 0; r < NR; ++r) buf[Swz<C>::f(a.idx(r))] = v[r];
+        compute_bar();
+        const GlobalAddr<RB> ga = linear_gaddr<RB>(h, tid);
+        C* __restrict__ dst = amps + tile_base(tile, h);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) dst[ga.at(r)] = buf[Swz<C>::f(r * kComputeThreads + tid)];
+        mbar_arrive(&empty[s]);
+      }
+    }
+  }
+}
+
+}  // namespace svb

@@ -34,17 +34,32 @@ struct OpDesc {
   int srt[kMaxK];     // tgt sorted ascending (zero-bit insertion order)
 };
 
+// Register-resident execution (k_reg_pass): a pass is a list of phases; in
+// phase p the register bits are R[0..RB) and ops [op_begin, op_end) act on
+// them (dense: OpDesc.pad = register-bit mask; diagonal: OpDesc.tgt[b] =
+// register index, or 16 + thread-bit index).
+constexpr int kMaxPhases = 32;
+enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2 };
+
+struct PhaseDesc {
+  int op_begin, op_end, flags, pad;
+  int R[4];
+};
+
 struct PassHeader {
   int T, L, m, n_ops;
   int high[kMaxHigh];
   int coeff_count;    // elements used in the pool
   int stages;
   long long n_tiles;
+  int n_phases;       // 0: k_tile_pass (ops use tile-local targets); >0: k_reg_pass
+  int reg_bits;       // RB of k_reg_pass
 };
 
 template <class C>
 struct PassArgs {
   PassHeader h;
+  PhaseDesc phases[kMaxPhases];
   OpDesc ops[kMaxOps];
   C coeff[kCoeffBytes / sizeof(C)];
 };
