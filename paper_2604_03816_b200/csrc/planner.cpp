@@ -206,6 +206,66 @@ bool build_phases(Pass& p, int RB, int prec) {
 
 }  // namespace
 
+// Decide the TMA tensor-map shape of a pass and the tile-local order of its
+// high bits (see Pass).  Includes as many runs of consecutive tile bits in the
+// box as fit a rank-5 tensor map; the remaining high bits are enumerated.
+void plan_tma(Pass& p, int n, int prec) {
+  const int sh = prec == SVB_C128 ? 1 : 0;
+  const int nw = n + sh;
+  std::vector<std::pair<int, int>> runs;  // qubit-space [start, len)
+  runs.push_back({0, p.L});
+  for (int b = 0; b < p.m; ++b) {
+    const int q = p.high[b];
+    if (runs.back().first + runs.back().second == q)
+      runs.back().second++;
+    else
+      runs.push_back({q, 1});
+  }
+  struct Dim { int start, bits, box; };
+  auto dims_for = [&](int k) {
+    std::vector<Dim> d;
+    int c = 0;
+    for (int r = 0; r < k; ++r) {
+      int st = runs[r].first == 0 ? 0 : runs[r].first + sh;
+      int len = runs[r].second + (runs[r].first == 0 ? sh : 0);
+      if (st > c) d.push_back({c, st - c, 0});
+      while (len > 0) {
+        int piece = std::min(len, 8);
+        d.push_back({st, piece, piece});
+        st += piece;
+        len -= piece;
+      }
+      c = st;
+    }
+    if (c < nw) d.push_back({c, nw - c, 0});
+    return d;
+  };
+  int k = int(runs.size());
+  while (k > 1 && int(dims_for(k).size()) > 5) --k;
+  std::vector<Dim> d = dims_for(k);
+  if (int(d.size()) > 5) {  // even the low run alone does not fit: 1-D bulk copies
+    p.tma_rank = 0;
+    p.n_enum = 0;
+  } else {
+    p.tma_rank = int(d.size());
+    for (int i = 0; i < p.tma_rank; ++i) {
+      p.tma_start[i] = d[i].start;
+      p.tma_bits[i] = d[i].bits;
+      p.tma_box[i] = d[i].box;
+    }
+    // tile-local order: included high runs first, enumerated ones last
+    std::vector<int> inc, exc;
+    for (int r = 1; r < int(runs.size()); ++r)
+      for (int j = 0; j < runs[r].second; ++j) (r < k ? inc : exc).push_back(runs[r].first + j);
+    int b = 0;
+    for (int q : inc) p.high[b++] = q;
+    for (int q : exc) p.high[b++] = q;
+    p.n_enum = int(exc.size());
+  }
+  for (int b = 0; b < p.m; ++b) p.high_sorted[b] = p.high[b];
+  std::sort(p.high_sorted, p.high_sorted + p.m);
+}
+
 bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const double* op_mats,
                 std::vector<Gate>& out, std::string& err) {
   out.clear();
@@ -396,6 +456,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       err = "internal planner error: tile set";
       return false;
     }
+    plan_tma(p, n, prec);
     auto local = [&](int q) {
       if (q < p.L) return q;
       for (int b = 0; b < p.m; ++b)

@@ -54,6 +54,14 @@ struct Pass {
   std::vector<KernelOp> ops;
   double cost = 0.0;
   int num_gates = 0;
+  int high_sorted[kMaxHigh] = {0};  // high[] ascending (tile_base insertion order)
+  // TMA tensor-map description of the tile (in 8-byte words; c128 adds the
+  // re/im bit 0).  Runs of consecutive tile bits are box dims; everything in
+  // between is a box-1 dim.  The last n_enum high bits are not in the box and
+  // are enumerated with one TMA load each (tile-local bits L+m-n_enum ..).
+  int tma_rank = 0;
+  int tma_start[5] = {0}, tma_bits[5] = {0}, tma_box[5] = {0};
+  int n_enum = 0;
   int reg_bits = 0;               // > 0: executed by k_reg_pass<RB = reg_bits>
   std::vector<RegPhase> phases;
   std::vector<RegOp> reg_ops;     // same order as ops

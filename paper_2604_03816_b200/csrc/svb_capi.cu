@@ -4,6 +4,8 @@
 // into __grid_constant__ kernel parameter blocks, launch geometry (persistent
 // grid = SMs x resident CTAs), error mapping.  No device memory is owned by a
 // plan; reductions use stream-ordered scratch (cudaMallocAsync).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -79,7 +81,18 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
   a.h.L = p.L;
   a.h.m = p.m;
   a.h.n_ops = int(p.ops.size());
-  for (int b = 0; b < p.m; ++b) a.h.high[b] = p.high[b];
+  for (int b = 0; b < p.m; ++b) {
+    a.h.high[b] = p.high[b];
+    a.h.high_sorted[b] = p.high_sorted[b];
+  }
+  a.h.tma_rank = p.tma_rank;
+  a.h.n_enum = p.n_enum;
+  for (int d = 0; d < 5; ++d) {
+    a.h.tma_start[d] = p.tma_start[d];
+    a.h.tma_bits[d] = p.tma_bits[d];
+    a.h.tma_box[d] = p.tma_box[d];
+  }
+  a.h.word_shift = sizeof(C) == 16 ? 1 : 0;
   a.h.stages = stages;
   a.h.n_phases = int(p.phases.size());
   a.h.reg_bits = p.reg_bits;
@@ -140,13 +153,48 @@ struct svb_plan {
 
 namespace {
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Tensor map over the whole shard viewed as 8-byte words, dims as planned.
+bool encode_tile_map(const PassHeader& h, void* amps, TensorMapBytes* out) {
+  auto enc = tensor_map_encoder();
+  if (!enc || h.tma_rank < 1) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  for (int d = 0; d < h.tma_rank; ++d) {
+    dims[d] = cuuint64_t(1) << h.tma_bits[d];
+    box[d] = 1u << h.tma_box[d];
+    estr[d] = 1;
+    if (d > 0) strides[d - 1] = (cuuint64_t(1) << h.tma_start[d]) * 8;
+  }
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_UINT64, cuuint32_t(h.tma_rank),
+                   amps, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <class C>
-int launch_pass(const PassArgs<C>& a0, int n_local, C* amps, cudaStream_t stream) {
+int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   DeviceFacts* f = nullptr;
   int rc = device_facts(&f);
   if (rc) return rc;
-  const PassArgs<C>& a = a0;
+  if (a.h.n_phases > 0 && a.h.tma_rank > 0 && !encode_tile_map(a.h, amps, &a.tmap)) {
+    // tensor map refused (should not happen for planned shapes): 1-D bulk copies
+    a.h.tma_rank = 0;
+  }
   const size_t smem = tile_pass_smem_bytes<C>(a.h);
+  static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
   void (*fn)(C*, PassArgs<C>);
   if (a.h.n_phases > 0) {
     fn = a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;

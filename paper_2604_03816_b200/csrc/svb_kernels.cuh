@@ -56,6 +56,34 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
       "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
+// Multi-dimensional TMA load (SASS UTMALDG) of one box into shared memory.
+__device__ __forceinline__ void tma_load(void* sdst, const void* tmap, const int* c, int rank, uint64_t* bar) {
+  const uint32_t d = smem_addr(sdst), b = smem_addr(bar);
+  const uint64_t m = reinterpret_cast<uint64_t>(tmap);
+  switch (rank) {
+    case 1:
+      asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
+                   ::"r"(d), "l"(m), "r"(c[0]), "r"(b) : "memory");
+      break;
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                   ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(b) : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                   ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b) : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                   ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b) : "memory");
+      break;
+    default:
+      asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                   ::"r"(d), "l"(m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b) : "memory");
+      break;
+  }
+}
+
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes, uint64_t policy) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
                "r"(smem_addr(ssrc)), "r"(bytes), "l"(policy)
@@ -204,7 +232,7 @@ __device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* po
 __device__ __forceinline__ long long tile_base(long long tile, const PassHeader& h) {
   long long g = tile << h.L;
   for (int b = 0; b < h.m; ++b) {
-    const int p = h.high[b];
+    const int p = h.high_sorted[b];
     g = ((g >> p) << (p + 1)) | (g & ((1LL << p) - 1));
   }
   return g;

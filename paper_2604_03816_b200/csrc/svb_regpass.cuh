@@ -111,40 +111,54 @@ __device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, con
   }
 }
 
-// Per-thread addressing of one phase: tile-local index of register rho is
-// base | sum_i bit_i(rho) << R[i]; thread bits are deposited at the non-R bits.
-template <int RB>
+// Per-thread addressing of one phase.  The tile-local index of register rho
+// is base | sum_i bit_i(rho) << R[i] (R ascending; base = tid with zero bits
+// inserted at R).  The swizzle is GF(2)-linear, so the swizzled address is
+// Swz(base) ^ (XOR of the uniform Swz(1 << R[i]) selected by rho): one LOP3
+// per amplitude.
+template <class C, int RB>
 struct PhaseAddr {
-  int base;
-  int offr[RB];
-  __device__ __forceinline__ PhaseAddr(const PhaseDesc& ph, int T, int tid) {
-    int used = 0;
+  int base, sbase;
+  int off[RB], soff[RB];
+  __device__ __forceinline__ PhaseAddr(const PhaseDesc& ph, int tid) {
+    int b = tid;
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
-      offr[i] = 1 << ph.R[i];
-      used |= offr[i];
+      const int r = ph.R[i];
+      b = ((b >> r) << (r + 1)) | (b & ((1 << r) - 1));
+      off[i] = 1 << r;
+      soff[i] = Swz<C>::f(off[i]);
     }
-    base = 0;
-    int k = 0;
-    for (int p = 0; p < T; ++p)
-      if (!((used >> p) & 1)) {
-        base |= ((tid >> k) & 1) << p;
-        ++k;
-      }
+    base = b;
+    sbase = Swz<C>::f(b);
   }
-  __device__ __forceinline__ int idx(int rho) const {
+  __device__ __forceinline__ int lin(int rho) const {
     int x = base;
 #pragma unroll
     for (int i = 0; i < RB; ++i)
-      if ((rho >> i) & 1) x += offr[i];
+      if ((rho >> i) & 1) x |= off[i];
     return x;
+  }
+  __device__ __forceinline__ int swz(int rho) const {
+    int x = 0;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if ((rho >> i) & 1) x ^= soff[i];
+    return sbase ^ x;
   }
 };
 
-// Tile-local bit p -> global (shard) bit: low bits map to themselves, bit L+b
-// to high[b].  Global offset of a tile-local index = tile_base + gthr + sum of
-// the register offsets selected by rho (<= RB 64-bit adds per amplitude).
+// Tile-local bit p -> global (shard) bit: low bits map to themselves, tile
+// bit L+b to high[b].  The map is linear, so a global offset is a per-thread
+// part plus a uniform part selected by rho.
 __device__ __forceinline__ int gpos(int p, const PassHeader& h) { return p < h.L ? p : h.high[p - h.L]; }
+
+__device__ __forceinline__ long long global_of(int x, const PassHeader& h) {
+  long long g = x & ((1 << h.L) - 1);
+  for (int b = 0; b < h.m; ++b)
+    if ((x >> (h.L + b)) & 1) g += 1LL << h.high[b];
+  return g;
+}
 
 template <int RB>
 struct GlobalAddr {
@@ -158,38 +172,6 @@ struct GlobalAddr {
     return x;
   }
 };
-
-// layout of phase `ph` (thread bits at the non-R tile bits)
-template <int RB>
-__device__ __forceinline__ GlobalAddr<RB> phase_gaddr(const PhaseDesc& ph, const PassHeader& h, int T, int tid) {
-  GlobalAddr<RB> g;
-  int used = 0;
-#pragma unroll
-  for (int i = 0; i < RB; ++i) {
-    g.goff[i] = 1LL << gpos(ph.R[i], h);
-    used |= 1 << ph.R[i];
-  }
-  g.gthr = 0;
-  int k = 0;
-  for (int p = 0; p < T; ++p)
-    if (!((used >> p) & 1)) {
-      if ((tid >> k) & 1) g.gthr += 1LL << gpos(p, h);
-      ++k;
-    }
-  return g;
-}
-
-// linear layout x = rho * 256 + tid (bits 0..7 from tid, 8.. from rho)
-template <int RB>
-__device__ __forceinline__ GlobalAddr<RB> linear_gaddr(const PassHeader& h, int tid) {
-  GlobalAddr<RB> g;
-#pragma unroll
-  for (int i = 0; i < RB; ++i) g.goff[i] = 1LL << gpos(8 + i, h);
-  g.gthr = 0;
-  for (int p = 0; p < 8; ++p)
-    if ((tid >> p) & 1) g.gthr += 1LL << gpos(p, h);
-  return g;
-}
 
 template <class C, int RB>
 __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
@@ -220,6 +202,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
   if (tid >= kComputeThreads) {
     // ------------------------------------------------ producer: TMA loads only
     const int lane = tid - kComputeThreads;
+    if (h.tma_rank > 0) {
+      // one tensor-map load per (enumerated) sub-box: a single UTMALDG per tile
+      // whenever the tile's qubit runs fit a rank-5 tensor map
+      if (lane != 0) return;
+      const int ne = h.n_enum;
+      const int sub = T - ne;
+      for (long long it = 0; it < mine; ++it) {
+        const int s = int(it % S);
+        if (it >= S) mbar_wait(&empty[s], uint32_t(((it - S) / S) & 1));
+        mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
+        const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
+        C* buf = tiles + (size_t(s) << T);
+        for (int e = 0; e < (1 << ne); ++e) {
+          long long origin = tb;
+          for (int j = 0; j < ne; ++j)
+            if ((e >> j) & 1) origin += 1LL << h.high[h.m - ne + j];
+          const long long w = origin << h.word_shift;
+          int c[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d)
+            c[d] = (d < h.tma_rank && h.tma_box[d] == 0) ? int((w >> h.tma_start[d]) & ((1LL << h.tma_bits[d]) - 1)) : 0;
+          tma_load(buf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[s]);
+        }
+      }
+      return;
+    }
     const int n_chunks = 1 << h.m;
     const uint32_t chunk_bytes = uint32_t(sizeof(C)) << h.L;
     const uint64_t pol = policy_evict_first();
@@ -239,6 +247,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
 
   // -------------------------------------------------------- compute threads
   const int np = h.n_phases;
+  // per-thread global offset of the linear layout x = rho * 256 + tid
+  GlobalAddr<RB> lin_g;
+  lin_g.gthr = global_of(tid, h);
+#pragma unroll
+  for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(8 + i, h);
   for (long long it = 0; it < mine; ++it) {
     const int s = int(it % S);
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
@@ -247,10 +260,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
     C v[NR];
     for (int p = 0; p < np; ++p) {
       const PhaseDesc& ph = args.phases[p];
-      const PhaseAddr<RB> a(ph, T, tid);
+      const PhaseAddr<C, RB> a(ph, tid);
+      const bool last = p == np - 1;
+      const bool tout = last && (ph.flags & PH_TRANSPOSE_OUT);
       if (p == 0) {
         if (ph.flags & PH_TRANSPOSE_IN) {
-          // linear (TMA) layout -> swizzled layout, contiguous conflict-free reads
+          // linear (TMA) layout -> swizzled layout through conflict-free reads
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[r * kComputeThreads + tid];
           compute_bar();
@@ -258,39 +273,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
           for (int r = 0; r < NR; ++r) buf[Swz<C>::f(r * kComputeThreads + tid)] = v[r];
           compute_bar();
 #pragma unroll
-          for (int r = 0; r < NR; ++r) v[r] = buf[Swz<C>::f(a.idx(r))];
+          for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
         } else {
 #pragma unroll
-          for (int r = 0; r < NR; ++r) v[r] = buf[a.idx(r)];
-          // all reads of the linear layout must finish before swizzled writes
-          if (np > 1 || (ph.flags & PH_TRANSPOSE_OUT)) compute_bar();
+          for (int r = 0; r < NR; ++r) v[r] = buf[a.lin(r)];
+          // all reads of the linear layout finish before swizzled writes
+          if (np > 1 || tout) compute_bar();
         }
       } else {
         compute_bar();
 #pragma unroll
-        for (int r = 0; r < NR; ++r) v[r] = buf[Swz<C>::f(a.idx(r))];
+        for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
-      const bool last = p == np - 1;
-      if (last && !(ph.flags & PH_TRANSPOSE_OUT)) mbar_arrive(&empty[s]);  // buffer free for the next load
+      if (last && !tout) mbar_arrive(&empty[s]);  // buffer free for the next load
       for (int o = ph.op_begin; o < ph.op_end; ++o) reg_apply<C, RB>(v, args.ops[o], pool, tid);
       if (!last) {
 #pragma unroll
-        for (int r = 0; r < NR; ++r) buf[Swz<C>::f(a.idx(r))] = v[r];
-      } else if (!(ph.flags & PH_TRANSPOSE_OUT)) {
-        // direct store from registers (coalesced when R avoids the lowest bits)
-        const GlobalAddr<RB> ga = phase_gaddr<RB>(ph, h, T, tid);
+        for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
+      } else if (!tout) {
+        // direct store from registers (coalesced: R avoids the bank-row bits)
+        GlobalAddr<RB> ga;
+        ga.gthr = global_of(a.base, h);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) ga.goff[i] = 1LL << gpos(ph.R[i], h);
         C* __restrict__ dst = amps + tile_base(tile, h);
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[ga.at(r)] = v[r];
       } else {
         // swizzled smem, then contiguous reads -> coalesced global stores
 #pragma unroll
-        for (int r = 0; r < NR; ++r) buf[Swz<C>::f(a.idx(r))] = v[r];
+        for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
         compute_bar();
-        const GlobalAddr<RB> ga = linear_gaddr<RB>(h, tid);
         C* __restrict__ dst = amps + tile_base(tile, h);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) dst[ga.at(r)] = buf[Swz<C>::f(r * kComputeThreads + tid)];
+        for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * kComputeThreads + tid)];
         mbar_arrive(&empty[s]);
       }
     }

@@ -54,10 +54,23 @@ struct PassHeader {
   long long n_tiles;
   int n_phases;       // 0: k_tile_pass (ops use tile-local targets); >0: k_reg_pass
   int reg_bits;       // RB of k_reg_pass
+  int high_sorted[kMaxHigh];
+  int tma_rank;       // 0: 1-D bulk copies per chunk; 1..5: one tensor load per enumerated sub-box
+  int n_enum;         // high bits L+m-n_enum.. are enumerated (2^n_enum tensor loads per tile)
+  int tma_start[5];   // word-bit start of each tensor dim (gap dims take coords from the origin)
+  int tma_bits[5];
+  int tma_box[5];     // log2 box extent (0 = box 1)
+  int word_shift;     // 0 for c64 (one 8-B word per amplitude), 1 for c128
+};
+
+// opaque 128-byte CUtensorMap (filled at launch time by the host)
+struct alignas(64) TensorMapBytes {
+  unsigned long long w[16];
 };
 
 template <class C>
 struct PassArgs {
+  TensorMapBytes tmap;
   PassHeader h;
   PhaseDesc phases[kMaxPhases];
   OpDesc ops[kMaxOps];

@@ -1,0 +1,373 @@
+"""State-vector sharding over P = 2^g GPUs with global-qubit swaps.
+
+The reference runs one process on one device and, when a state does not fit,
+falls back to the CPU (ref ``pkg/src/aqsim/memory.py:290-340``).  Here the
+state is partitioned instead: rank r holds the 2^(n-g) amplitudes whose top g
+*physical* index bits equal r, so physical qubits n-g..n-1 are "global".
+
+The scheduler keeps a logical<->physical qubit permutation (allowed by the
+reference contract that engines may swap buffers between gates,
+ref ``circuit.py:189-194``):
+
+* a *local segment* is every pending gate whose qubits are all local and that
+  no deferred gate must precede (same dependency rule as the planner); it runs
+  as one planned sequence of tile passes on each shard;
+* a *swap* brings the global qubits the next deferred gates need into the top
+  m local positions: each rank splits its shard into 2^m contiguous blocks by
+  those m bits and exchanges block w with the rank whose global bits equal w
+  (an all-to-all inside groups of 2^m ranks; the rank's own block stays);
+* victims (local qubits sent out) are the ones used furthest in the future;
+  they are moved to the top local positions by physical SWAP gates folded into
+  the preceding segment, and the *initial* layout is chosen so that the first
+  swap needs none (|0...0> is invariant under qubit relabelling).
+
+Transport is ``torch.distributed`` point-to-point (NCCL over NVLink on the
+GPU box, gloo in the CPU tests), chunked through a double-buffered staging
+area so the copy-back of chunk c overlaps the transfer of chunk c+1.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .circuit import GateKind, GateOp, Precision, as_precision, effective_unitary
+
+
+# --------------------------------------------------------------- scheduling
+
+@dataclass
+class LocalStep:
+    gates: list                      # GateOps with PHYSICAL local targets
+
+
+@dataclass
+class SwapStep:
+    global_pos: list                 # physical global positions (ascending), each >= n_local
+    n_local: int
+
+    @property
+    def m(self) -> int:
+        return len(self.global_pos)
+
+    @property
+    def local_pos(self) -> list:
+        return [self.n_local - self.m + i for i in range(self.m)]
+
+
+@dataclass
+class Schedule:
+    n: int
+    g: int
+    initial_layout: list             # phys_of[logical]
+    final_layout: list
+    steps: list = field(default_factory=list)
+
+    @property
+    def n_local(self) -> int:
+        return self.n - self.g
+
+    def num_swaps(self) -> int:
+        return sum(isinstance(s, SwapStep) for s in self.steps)
+
+
+def _physical_op(op, phys_of) -> GateOp:
+    return GateOp(GateKind.CUSTOM, tuple(phys_of[t] for t in op.targets), (), effective_unitary(op))
+
+
+def _schedule_once(gates, n: int, g: int, layout: list) -> tuple[Schedule, list]:
+    nl = n - g
+    phys_of = list(layout)
+    log_at = [0] * n
+    for q, p in enumerate(phys_of):
+        log_at[p] = q
+    sched = Schedule(n, g, list(layout), [])
+    pending = list(range(len(gates)))
+    first_victims: list = []
+    while pending:
+        blocked: set = set()
+        seg, deferred = [], []
+        for i in pending:
+            tg = gates[i].targets
+            if any(t in blocked for t in tg) or any(phys_of[t] >= nl for t in tg):
+                deferred.append(i)
+                blocked.update(tg)
+            else:
+                seg.append(_physical_op(gates[i], phys_of))
+        if seg:
+            sched.steps.append(LocalStep(seg))
+        if not deferred:
+            break
+        # global logical qubits the deferred gates need, in first-use order
+        need: list = []
+        for i in deferred:
+            for t in gates[i].targets:
+                if phys_of[t] >= nl and t not in need:
+                    need.append(t)
+        m = min(len(need), g)
+        need = need[:m]
+        first_tg = set(gates[deferred[0]].targets)
+        if not set(t for t in first_tg if phys_of[t] >= nl) <= set(need):
+            raise RuntimeError("scheduler: first deferred gate needs more global qubits than exist")
+        # victims: local logical qubits not needed by the first deferred gate,
+        # with the furthest next use
+        next_use = {}
+        for pos, i in enumerate(deferred):
+            for t in gates[i].targets:
+                next_use.setdefault(t, pos)
+        cands = [log_at[p] for p in range(nl) if log_at[p] not in first_tg]
+        if len(cands) < m:
+            raise ValueError("not enough local qubits for a global swap (n_local too small)")
+        cands.sort(key=lambda q: (-next_use.get(q, len(deferred) + 1), -phys_of[q]))
+        victims = cands[:m]
+        if not first_victims:
+            first_victims = list(victims)
+        top = [nl - m + i for i in range(m)]
+        # move victims onto the top local positions with physical SWAPs
+        fix = []
+        placed = [v for v in victims if phys_of[v] in top]
+        free_top = [p for p in top if log_at[p] not in placed]
+        for v in victims:
+            if v in placed:
+                continue
+            p_dst = free_top.pop(0)
+            a, b = phys_of[v], p_dst
+            fix.append(GateOp(GateKind.SWAP, (min(a, b), max(a, b))))
+            qa, qb = log_at[a], log_at[b]
+            phys_of[qa], phys_of[qb] = b, a
+            log_at[a], log_at[b] = qb, qa
+        if fix:
+            if sched.steps and isinstance(sched.steps[-1], LocalStep):
+                sched.steps[-1].gates.extend(fix)
+            else:
+                sched.steps.append(LocalStep(fix))
+        # pair victim at top position i with the i-th ascending global position
+        gpos = sorted(phys_of[q] for q in need)
+        sched.steps.append(SwapStep(gpos, nl))
+        for i, gp in enumerate(gpos):
+            lp = nl - m + i
+            qa, qb = log_at[lp], log_at[gp]
+            phys_of[qa], phys_of[qb] = gp, lp
+            log_at[lp], log_at[gp] = qb, qa
+        pending = deferred
+    sched.final_layout = list(phys_of)
+    return sched, first_victims
+
+
+def schedule(circuit, world_size: int, optimise_layout: bool = True) -> Schedule:
+    """Lower a (fused) circuit into local segments and global swaps."""
+    n = circuit.num_qubits
+    g = int(round(math.log2(world_size)))
+    if 1 << g != world_size:
+        raise ValueError("world size must be a power of two")
+    if g > n - 1:
+        raise ValueError("too many ranks for the qubit count")
+    gates = list(circuit.gates)
+    ident = list(range(n))
+    sched, victims = _schedule_once(gates, n, g, ident)
+    if g == 0 or not optimise_layout or not victims:
+        return sched
+    # initial layout: first-swap victims start on the top local positions
+    layout = list(ident)
+    log_at = list(range(n))
+    nl = n - g
+    top = [nl - len(victims) + i for i in range(len(victims))]
+    for v, p_dst in zip(victims, top):
+        a = layout[v]
+        if a == p_dst:
+            continue
+        qb = log_at[p_dst]
+        layout[v], layout[qb] = p_dst, a
+        log_at[a], log_at[p_dst] = qb, v
+    better, _ = _schedule_once(gates, n, g, layout)
+    swaps_a = sum(len(s.gates) for s in sched.steps if isinstance(s, LocalStep))
+    swaps_b = sum(len(s.gates) for s in better.steps if isinstance(s, LocalStep))
+    if (better.num_swaps(), swaps_b) <= (sched.num_swaps(), swaps_a):
+        return better
+    return sched
+
+
+def block_peer(rank: int, step: SwapStep, w: int) -> int:
+    """Rank that exchanges block w with `rank` in a swap."""
+    r = rank
+    for i, gp in enumerate(step.global_pos):
+        j = gp - step.n_local
+        r = (r & ~(1 << j)) | (((w >> i) & 1) << j)
+    return r
+
+
+def own_block(rank: int, step: SwapStep) -> int:
+    return sum(((rank >> (gp - step.n_local)) & 1) << i for i, gp in enumerate(step.global_pos))
+
+
+def unpermute(full_physical: np.ndarray, n: int, phys_of: list) -> np.ndarray:
+    """Physical-order amplitudes -> logical little-endian order."""
+    t = full_physical.reshape((2,) * n)          # axis a <-> physical bit n-1-a
+    # logical axis order (big-endian): logical bit n-1-a' at axis a'
+    axes = [n - 1 - phys_of[n - 1 - a] for a in range(n)]
+    return np.ascontiguousarray(t.transpose(axes)).reshape(-1)
+
+
+# ----------------------------------------------------------------- execution
+
+class CudaShardBackend:
+    """Local work on a shard through libsvb200 (the product path)."""
+
+    def __init__(self, device, options=None):
+        import torch
+        from .b200 import B200Engine
+        self.torch = torch
+        self.engine = B200Engine("b200-shard", device=device, options=options)
+        self.device = self.engine.device
+
+    def alloc(self, n_local: int, precision):
+        state = self.engine.init_state(n_local, precision)
+        return state
+
+    def fill(self, state, index_of_one: int):
+        import ctypes as C
+        from . import _native
+        from .b200 import prec_code
+        _native.check(_native.lib().svb_fill_basis(
+            C.c_void_p(state.tensor.data_ptr()), state.num_qubits, prec_code(state.precision),
+            index_of_one, C.c_void_p(self.engine.stream())))
+        state.touch()
+
+    def plan(self, n_local: int, precision, gates):
+        from .b200 import CircuitPlan
+        return CircuitPlan(n_local, precision, gates, self.engine.options)
+
+    def run(self, state, plan):
+        self.engine.execute(state, plan)
+
+    def tensor(self, state):
+        return state.tensor
+
+    def norm2(self, state) -> float:
+        return self.engine.norm_squared(state)
+
+    def synchronize(self):
+        self.engine.synchronize()
+
+
+class ShardedEngine:
+    """Runs circuits on a state sharded over the torch.distributed world."""
+
+    def __init__(self, backend, group=None, chunk_elems: int = 1 << 24):
+        import torch.distributed as dist
+        self.dist = dist
+        self.backend = backend
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.chunk_elems = chunk_elems
+        self._staging = None
+
+    # -------------------------------------------------------------- program
+    def compile(self, circuit, precision=Precision.DOUBLE):
+        precision = as_precision(precision)
+        sched = schedule(circuit, self.world)
+        progs = []
+        for st in sched.steps:
+            if isinstance(st, LocalStep):
+                progs.append(("local", self.backend.plan(sched.n_local, precision, st.gates)))
+            else:
+                progs.append(("swap", st))
+        return sched, progs
+
+    def init_state(self, n_local: int, precision):
+        state = self.backend.alloc(n_local, precision)
+        self.backend.fill(state, 0 if self.rank == 0 else -1)
+        return state
+
+    def run_program(self, state, progs):
+        for kind, obj in progs:
+            if kind == "local":
+                self.backend.run(state, obj)
+            else:
+                self.exchange(state, obj)
+        return state
+
+    def run_circuit(self, circuit, precision=Precision.DOUBLE):
+        sched, progs = self.compile(circuit, precision)
+        state = self.init_state(sched.n_local, precision)
+        self.run_program(state, progs)
+        self.backend.synchronize()
+        return ShardedState(self, state, sched)
+
+    # ------------------------------------------------------------- exchange
+    def _staging_for(self, t, elems: int):
+        if self._staging is None or self._staging.numel() < elems or self._staging.dtype != t.dtype \
+                or self._staging.device != t.device:
+            self._staging = t.new_empty(elems)
+        return self._staging[:elems]
+
+    def exchange(self, state, step: SwapStep):
+        """Swap the step's global qubits with the top m local qubits (in place)."""
+        dist = self.dist
+        t = self.backend.tensor(state)
+        nl = step.n_local
+        m = step.m
+        blk = 1 << (nl - m)
+        chunk = min(blk, self.chunk_elems)
+        n_chunks = blk // chunk
+        mine = own_block(self.rank, step)
+        peers = [(w, block_peer(self.rank, step, w)) for w in range(1 << m) if w != mine]
+        if not peers:
+            return
+        npeer = len(peers)
+        stage = self._staging_for(t, 2 * npeer * chunk).view(2, npeer, chunk)
+
+        def issue(c):
+            ops = []
+            for k, (w, peer) in enumerate(peers):
+                src = t[w * blk + c * chunk: w * blk + (c + 1) * chunk]
+                ops.append(dist.P2POp(dist.isend, src, peer, self.group))
+                ops.append(dist.P2POp(dist.irecv, stage[c % 2, k], peer, self.group))
+            return dist.batch_isend_irecv(ops)
+
+        inflight = issue(0)
+        for c in range(n_chunks):
+            nxt = issue(c + 1) if c + 1 < n_chunks else None
+            for r in inflight:
+                r.wait()
+            for k, (w, _peer) in enumerate(peers):
+                t[w * blk + c * chunk: w * blk + (c + 1) * chunk].copy_(stage[c % 2, k])
+            inflight = nxt
+        if hasattr(state, "touch"):
+            state.touch()
+
+
+class ShardedState:
+    """Handle on a sharded result: device reductions and (small n) gathering."""
+
+    def __init__(self, engine: ShardedEngine, state, sched: Schedule):
+        self.engine = engine
+        self.state = state
+        self.schedule = sched
+        self.num_qubits = sched.n
+
+    def norm_squared(self) -> float:
+        import torch
+        v = torch.tensor([self.engine.backend.norm2(self.state)], dtype=torch.float64)
+        self.engine.dist.all_reduce(v, group=self.engine.group)
+        return float(v.item())
+
+    def gather(self) -> np.ndarray | None:
+        """Full logical-order state on rank 0 (None elsewhere); for modest n."""
+        import torch
+        dist = self.engine.dist
+        t = self.engine.backend.tensor(self.state).detach()
+        host = t.cpu() if t.device.type != "cpu" else t
+        if dist.get_backend(self.engine.group) == "nccl":
+            parts = [torch.empty_like(t) for _ in range(self.engine.world)]
+            dist.all_gather(parts, t, group=self.engine.group)
+            parts = [p.cpu() for p in parts]
+        else:
+            parts = [torch.empty_like(host) for _ in range(self.engine.world)]
+            dist.all_gather(parts, host.contiguous(), group=self.engine.group)
+        if self.engine.rank != 0:
+            return None
+        full = torch.cat(parts).numpy()
+        return unpermute(full, self.schedule.n, self.schedule.final_layout)

@@ -24,7 +24,7 @@ def tile_indices(n: int, info: dict, tile: int) -> np.ndarray:
     """Global amplitude index of every tile-local index (the kernel's addressing)."""
     L, high, T = info["low_bits"], info["high"], info["tile_bits"]
     g = tile << L
-    for p in high:
+    for p in sorted(high):
         g = ((g >> p) << (p + 1)) | (g & ((1 << p) - 1))
     local = np.arange(1 << T)
     idx = np.full(1 << T, g, dtype=np.int64) + (local & ((1 << L) - 1))
