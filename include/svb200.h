@@ -107,7 +107,10 @@ int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k,
 /* Register phase `phase` of pass `pass`: R[4] register bits, op range, flags. */
 int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_begin, int* op_end,
                    int* flags);
-/* Register-phase encoding of kernel op i: dense -> *mask, diagonal -> src[k]. */
+/* Register-phase encoding of kernel op i.  Dense: *mask = register-bit mask.
+ * Diagonal: *mask = kt, src[0..kt) = thread bits of table bits kr..; src must
+ * hold SVB_MAX_TARGETS + 2 ints, src[8..9] = the 64-bit map rho -> register
+ * part of the table index (4 bits per rho). */
 int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
                       double* coeffs, int coeff_cap);
 int svb_plan_execute(svb_plan* plan, void* amps, void* stream);

@@ -151,12 +151,16 @@ class NativePlan:
 
     def phase_op(self, p: int, i: int) -> dict:
         kind, k, mask = C.c_int(), C.c_int(), C.c_int()
-        src = np.zeros(SVB_MAX_TARGETS, dtype=np.int32)
+        src = np.zeros(SVB_MAX_TARGETS + 2, dtype=np.int32)
         co = np.zeros(2 * 4096, dtype=np.float64)
         n = check(lib().svb_plan_phase_op(self._h, p, i, C.byref(kind), C.byref(k), C.byref(mask),
                                           _iptr(src), _dptr(co), 4096))
-        return {"kind": "diag" if kind.value == 1 else "dense", "k": k.value, "mask": mask.value,
-                "src": [int(x) for x in src[:k.value]], "coeffs": co[:2 * n].view(np.complex128).copy()}
+        out = {"kind": "diag" if kind.value == 1 else "dense", "k": k.value, "mask": mask.value,
+               "coeffs": co[:2 * n].view(np.complex128).copy()}
+        if kind.value == 1:
+            out["thread_bits"] = [int(x) for x in src[:mask.value]]
+            out["rmap"] = int(np.uint32(src[8])) | (int(np.uint32(src[9])) << 32)
+        return out
 
     def pass_gates(self, p: int) -> list[int]:
         buf = np.zeros(max(1, self.num_gates), dtype=np.int32)

@@ -107,42 +107,80 @@ struct DiagAcc {
 
 size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 
-// Partition a lowered pass into register phases (k_reg_pass).  Dense ops are
-// kept in program order; a new phase starts when the union of register bits
-// would exceed RB.  Diagonal ops ride in whatever phase is current.  Returns
-// false when the pass must use the shared-memory kernel instead.
+// Partition a lowered pass into register phases (k_reg_pass).  Phases are
+// list-scheduled: each phase scans the remaining ops in order and takes every
+// op whose predecessors (earlier ops on a shared bit, diagonal pairs excepted)
+// are already scheduled and whose bits fit the phase's RB register bits
+// (diagonal ops fit any phase).  Ops are reordered into phase order.
+// Returns false when the pass must use the shared-memory kernel instead.
 bool build_phases(Pass& p, int RB, int prec) {
   if (RB < 1 || RB > 4 || p.T != RB + 8) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
-  std::vector<std::vector<int>> sets;
-  std::vector<std::pair<int, int>> ranges;
-  std::vector<int> cur;
-  int begin = 0;
-  for (int i = 0; i < int(p.ops.size()); ++i) {
-    const KernelOp& op = p.ops[i];
-    if (op.kind == OP_DIAG) continue;
-    std::vector<int> u = cur;
-    for (int j = 0; j < op.k; ++j)
-      if (std::find(u.begin(), u.end(), op.tgt[j]) == u.end()) u.push_back(op.tgt[j]);
-    if (int(u.size()) <= RB) {
-      cur.swap(u);
-    } else {
-      sets.push_back(cur);
-      ranges.emplace_back(begin, i);
-      begin = i;
-      cur.assign(op.tgt, op.tgt + op.k);
+  for (const KernelOp& op : p.ops)
+    if (op.kind == OP_DIAG && op.k > kMaxK) return false;
+  std::vector<int> pending(p.ops.size());
+  for (size_t i = 0; i < p.ops.size(); ++i) pending[i] = int(i);
+  std::vector<std::vector<int>> sets, members;
+  while (!pending.empty()) {
+    std::vector<char> block_all(p.T, 0), block_dense(p.T, 0);
+    std::vector<int> R, took, rest;
+    for (int i : pending) {
+      const KernelOp& op = p.ops[i];
+      bool blocked = false;
+      for (int j = 0; j < op.k && !blocked; ++j)
+        blocked = block_all[op.tgt[j]] || (op.kind == OP_DENSE && block_dense[op.tgt[j]]);
+      bool take = false;
+      if (!blocked) {
+        if (op.kind == OP_DIAG) {
+          take = true;
+        } else {
+          std::vector<int> u = R;
+          for (int j = 0; j < op.k; ++j)
+            if (std::find(u.begin(), u.end(), op.tgt[j]) == u.end()) u.push_back(op.tgt[j]);
+          if (int(u.size()) <= RB) {
+            R.swap(u);
+            take = true;
+          }
+        }
+      }
+      if (take) {
+        took.push_back(i);
+      } else {
+        rest.push_back(i);
+        for (int j = 0; j < op.k; ++j) (op.kind == OP_DIAG ? block_dense : block_all)[op.tgt[j]] = 1;
+      }
     }
+    sets.push_back(R);
+    members.push_back(took);
+    pending.swap(rest);
   }
-  sets.push_back(cur);
-  ranges.emplace_back(begin, int(p.ops.size()));
   if (int(sets.size()) > kMaxPhases) return false;
+  // reorder ops into phase order
+  std::vector<KernelOp> ordered;
+  std::vector<std::pair<int, int>> ranges;
+  for (auto& mem : members) {
+    const int b = int(ordered.size());
+    for (int i : mem) ordered.push_back(p.ops[i]);
+    ranges.emplace_back(b, int(ordered.size()));
+  }
+  p.ops.swap(ordered);
+
   const int low_conflict = prec == SVB_C64 ? 4 : 3;  // bank-row index bits
   p.phases.clear();
   p.reg_ops.assign(p.ops.size(), RegOp());
   for (size_t ph = 0; ph < sets.size(); ++ph) {
     std::vector<int> R = sets[ph];
-    for (int b = p.T - 1; b >= 0 && int(R.size()) < RB; --b)  // fill with high tile bits
+    // fill free register bits: prefer bits of this phase's diagonal ops (fewer
+    // thread-sourced table bits), then the highest tile bits (coalescing)
+    for (int i = ranges[ph].first; i < ranges[ph].second && int(R.size()) < RB; ++i) {
+      const KernelOp& op = p.ops[i];
+      if (op.kind != OP_DIAG) continue;
+      for (int j = op.k - 1; j >= 0 && int(R.size()) < RB; --j)
+        if (op.tgt[j] >= low_conflict && std::find(R.begin(), R.end(), op.tgt[j]) == R.end())
+          R.push_back(op.tgt[j]);
+    }
+    for (int b = p.T - 1; b >= 0 && int(R.size()) < RB; --b)
       if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
     std::sort(R.begin(), R.end());
     RegPhase rp;
@@ -169,11 +207,34 @@ bool build_phases(Pass& p, int RB, int prec) {
       ro.kind = op.kind;
       ro.k = op.k;
       if (op.kind == OP_DIAG) {
+        // new table index = [register-sourced bits asc. by register | thread bits asc.]
+        std::vector<std::pair<int, int>> regb, thrb;  // (register idx / thread bit, op bit)
         for (int b = 0; b < op.k; ++b) {
           const int r = reg_of(op.tgt[b]);
-          ro.src[b] = r >= 0 ? r : 16 + thread_bit_of(op.tgt[b]);
+          if (r >= 0)
+            regb.push_back({r, b});
+          else
+            thrb.push_back({thread_bit_of(op.tgt[b]), b});
         }
-        ro.coeff = op.coeff;
+        std::sort(regb.begin(), regb.end());
+        std::sort(thrb.begin(), thrb.end());
+        const int kr = int(regb.size()), kt = int(thrb.size());
+        ro.mask = kt;  // stored in OpDesc.pad
+        for (int j = 0; j < kt; ++j) ro.src[j] = thrb[j].first;
+        unsigned long long rmap = 0;
+        for (int rho = 0; rho < (1 << RB); ++rho) {
+          int d = 0;
+          for (int j = 0; j < kr; ++j) d |= ((rho >> regb[j].first) & 1) << j;
+          rmap |= static_cast<unsigned long long>(d) << (4 * rho);
+        }
+        ro.rmap = rmap;
+        ro.coeff.assign(op.coeff.size(), cd());
+        for (size_t nidx = 0; nidx < op.coeff.size(); ++nidx) {
+          int old = 0;
+          for (int j = 0; j < kr; ++j) old |= ((int(nidx) >> j) & 1) << regb[j].second;
+          for (int j = 0; j < kt; ++j) old |= ((int(nidx) >> (kr + j)) & 1) << thrb[j].second;
+          ro.coeff[nidx] = op.coeff[old];
+        }
       } else {
         int ri[kMaxK];
         for (int j = 0; j < op.k; ++j) {

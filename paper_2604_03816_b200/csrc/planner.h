@@ -43,8 +43,9 @@ struct RegPhase {
 struct RegOp {
   int kind = OP_DENSE;
   int k = 0;
-  int mask = 0;            // dense: register-bit mask
-  int src[kMaxK] = {0};    // diagonal: register index, or 16 + thread-bit index
+  int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
+  int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
+  unsigned long long rmap = 0;  // diagonal: 4-bit register part of the table index per rho
   std::vector<cd> coeff;   // dense: matrix permuted to ascending register bits
 };
 

@@ -114,7 +114,11 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
       d.k = ro.k;
       d.coeff_off = off;
       d.pad = ro.mask;
-      for (int j = 0; j < ro.k; ++j) d.tgt[j] = ro.src[j];
+      if (ro.kind == OP_DIAG) {
+        d.tgt[0] = int(static_cast<unsigned>(ro.rmap & 0xffffffffull));
+        d.tgt[1] = int(static_cast<unsigned>(ro.rmap >> 32));
+        for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
+      }
       for (const cd& z : ro.coeff) {
         a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
         a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
@@ -376,7 +380,11 @@ int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, 
   *kind = op.kind;
   *k = op.k;
   *mask = op.mask;
-  for (int j = 0; j < op.k; ++j) src[j] = op.src[j];
+  for (int j = 0; j < kMaxK; ++j) src[j] = op.src[j];
+  if (op.kind == OP_DIAG) {  // src[8], src[9] carry the 64-bit register map
+    src[8] = int(static_cast<unsigned>(op.rmap & 0xffffffffull));
+    src[9] = int(static_cast<unsigned>(op.rmap >> 32));
+  }
   if (coeffs) {
     if (int(op.coeff.size()) > coeff_cap) return fail(SVB_EINVAL, "coefficient capacity too small");
     for (size_t e = 0; e < op.coeff.size(); ++e) {

@@ -65,29 +65,24 @@ __device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__
   }
 }
 
-// Diagonal op: table index bit b comes from register bit (src<16) or thread bit (src-16).
+// Diagonal op.  The planner orders the table index as [register-sourced bits
+// | thread-sourced bits]: rmap packs, per register index rho, the register
+// part of the table index (4 bits per rho); the thread part is gathered once
+// per tile from the thread bits listed in op.srt[0..kt).
 template <class C, int RB>
 __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, const C* __restrict__ table, int tid) {
+  const int kt = op.pad;
+  const int kr = op.k - kt;
   int dt = 0;
-  int contrib[RB];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) contrib[i] = 0;
-  for (int b = 0; b < op.k; ++b) {
-    const int src = op.tgt[b];
-    if (src >= 16)
-      dt |= ((tid >> (src - 16)) & 1) << b;
-    else {
-#pragma unroll
-      for (int i = 0; i < RB; ++i)
-        if (i == src) contrib[i] = 1 << b;
-    }
-  }
+  for (int j = 0; j < kMaxK; ++j)
+    if (j < kt) dt |= ((tid >> op.srt[j]) & 1) << j;
+  dt <<= kr;
+  const unsigned long long rmap =
+      (static_cast<unsigned long long>(static_cast<unsigned>(op.tgt[1])) << 32) | static_cast<unsigned>(op.tgt[0]);
 #pragma unroll
   for (int rho = 0; rho < (1 << RB); ++rho) {
-    int d = dt;
-#pragma unroll
-    for (int i = 0; i < RB; ++i)
-      if ((rho >> i) & 1) d |= contrib[i];
+    const int d = dt | int((rmap >> (4 * rho)) & 15);
     v[rho] = cmul(v[rho], table[d]);
   }
 }
@@ -208,9 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
       if (lane != 0) return;
       const int ne = h.n_enum;
       const int sub = T - ne;
+      int s = 0;
+      uint32_t ph = 0;  // parity of the use of buffer s
       for (long long it = 0; it < mine; ++it) {
-        const int s = int(it % S);
-        if (it >= S) mbar_wait(&empty[s], uint32_t(((it - S) / S) & 1));
+        if (it >= S) mbar_wait(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
         const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
         C* buf = tiles + (size_t(s) << T);
@@ -224,6 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
           for (int d = 0; d < 5; ++d)
             c[d] = (d < h.tma_rank && h.tma_box[d] == 0) ? int((w >> h.tma_start[d]) & ((1LL << h.tma_bits[d]) - 1)) : 0;
           tma_load(buf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[s]);
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
         }
       }
       return;
@@ -252,11 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
   lin_g.gthr = global_of(tid, h);
 #pragma unroll
   for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(8 + i, h);
-  for (long long it = 0; it < mine; ++it) {
-    const int s = int(it % S);
+  int s = 0;
+  uint32_t parity = 0;
+  for (long long it = 0; it < mine; ++it, (++s == S ? (s = 0, parity ^= 1) : 0)) {
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
-    mbar_wait(&full[s], uint32_t((it / S) & 1));
+    mbar_wait(&full[s], parity);
     C v[NR];
     for (int p = 0; p < np; ++p) {
       const PhaseDesc& ph = args.phases[p];

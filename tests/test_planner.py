@@ -195,17 +195,14 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                             for i in range(d):
                                 v[:, cols[i]] = vin @ M[i]
                     else:
+                        kt = op["mask"]
+                        kr = op["k"] - kt
                         dt = np.zeros(256, dtype=np.int64)
-                        contrib = [0] * rb
-                        for b, src in enumerate(op["src"]):
-                            if src >= 16:
-                                dt |= ((tid >> (src - 16)) & 1) << b
-                            else:
-                                contrib[src] = 1 << b
+                        for j, tb in enumerate(op["thread_bits"]):
+                            dt |= ((tid >> tb) & 1) << (kr + j)
                         tab = op["coeffs"].astype(v.dtype)
                         for rho in range(nr):
-                            dd = dt | sum(contrib[i] for i in range(rb) if (rho >> i) & 1)
-                            v[:, rho] *= tab[dd]
+                            v[:, rho] *= tab[dt | ((op["rmap"] >> (4 * rho)) & 15)]
                 buf[loc] = v
             amps[idx] = buf
     return amps
