@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--min-low-bits", type=int, default=0)
     ap.add_argument("--reg-bits", type=int, default=0)
     ap.add_argument("--no-reg-phases", action="store_true")
+    ap.add_argument("--pass-times", action="store_true", help="print per-pass device times to stderr")
     return ap.parse_args()
 
 
@@ -274,6 +275,15 @@ def run_b200(args):
     total_ms = start.elapsed_time(stop)
     pass_ms = [sum(ev[k][p][0].elapsed_time(ev[k][p][1]) for k in range(args.steps)) / args.steps
                for p in range(n_passes)]
+    if args.pass_times:
+        for p_, ms_ in enumerate(pass_ms):
+            info = plan.native.pass_info(p_)
+            ops = [plan.native.kernel_op(p_, i)["kind"][0] + str(plan.native.kernel_op(p_, i)["k"])
+                   for i in range(info["num_kernel_ops"])]
+            fl = [plan.native.phase(p_, f)["flags"] for f in range(info["num_phases"])]
+            print(f"pass {p_:3d} {ms_:.3f} ms frac {2 * (1 << n) * precision.amplitude_bytes / ms_ / 1e6 / 6548:.2f} "
+                  f"L={info['low_bits']} high={info['high']} phases={info['num_phases']} flags={fl} "
+                  f"ops={ops} est={info['est_cost']:.2f}", file=sys.stderr)
     ms_step = total_ms / args.steps
     value = g0 / (ms_step / 1e3)
     norm = eng.norm_squared(state)

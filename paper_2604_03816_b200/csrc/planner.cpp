@@ -283,10 +283,12 @@ void plan_tma(Pass& p, int n, int prec) {
       runs.push_back({q, 1});
   }
   struct Dim { int start, bits, box; };
-  auto dims_for = [&](int k) {
+  // dims for the subset `inc` (bit r set: run r is a box dim; run 0 always)
+  auto dims_for = [&](unsigned inc) {
     std::vector<Dim> d;
     int c = 0;
-    for (int r = 0; r < k; ++r) {
+    for (int r = 0; r < int(runs.size()); ++r) {
+      if (!((inc >> r) & 1)) continue;
       int st = runs[r].first == 0 ? 0 : runs[r].first + sh;
       int len = runs[r].second + (runs[r].first == 0 ? sh : 0);
       if (st > c) d.push_back({c, st - c, 0});
@@ -301,13 +303,25 @@ void plan_tma(Pass& p, int n, int prec) {
     if (c < nw) d.push_back({c, nw - c, 0});
     return d;
   };
-  int k = int(runs.size());
-  while (k > 1 && int(dims_for(k).size()) > 5) --k;
-  std::vector<Dim> d = dims_for(k);
-  if (int(d.size()) > 5) {  // even the low run alone does not fit: 1-D bulk copies
+  // choose the subset of runs that fits rank 5 with the fewest enumerated bits
+  const int nr = int(runs.size());
+  unsigned best = 0;
+  int best_excl = 1 << 30;
+  for (unsigned inc = 1; inc < (1u << nr); inc += 2) {  // run 0 always included
+    if (int(dims_for(inc).size()) > 5) continue;
+    int excl = 0;
+    for (int r = 0; r < nr; ++r)
+      if (!((inc >> r) & 1)) excl += runs[r].second;
+    if (excl < best_excl) {
+      best_excl = excl;
+      best = inc;
+    }
+  }
+  if (best == 0 || best_excl > 6) {  // no usable tensor map: 1-D bulk copies per chunk
     p.tma_rank = 0;
     p.n_enum = 0;
   } else {
+    std::vector<Dim> d = dims_for(best);
     p.tma_rank = int(d.size());
     for (int i = 0; i < p.tma_rank; ++i) {
       p.tma_start[i] = d[i].start;
@@ -316,8 +330,8 @@ void plan_tma(Pass& p, int n, int prec) {
     }
     // tile-local order: included high runs first, enumerated ones last
     std::vector<int> inc, exc;
-    for (int r = 1; r < int(runs.size()); ++r)
-      for (int j = 0; j < runs[r].second; ++j) (r < k ? inc : exc).push_back(runs[r].first + j);
+    for (int r = 1; r < nr; ++r)
+      for (int j = 0; j < runs[r].second; ++j) (((best >> r) & 1) ? inc : exc).push_back(runs[r].first + j);
     int b = 0;
     for (int q : inc) p.high[b++] = q;
     for (int q : exc) p.high[b++] = q;

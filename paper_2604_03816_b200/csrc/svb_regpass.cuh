@@ -169,7 +169,7 @@ struct GlobalAddr {
 };
 
 template <class C, int RB>
-__global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+__global__ void __launch_bounds__(kThreads, 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + 8;
   constexpr int NR = 1 << RB;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
       int s = 0;
       uint32_t ph = 0;  // parity of the use of buffer s
       for (long long it = 0; it < mine; ++it) {
-        if (it >= S) mbar_wait(&empty[s], ph ^ 1);
+        if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
         const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
         C* buf = tiles + (size_t(s) << T);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_reg_pass(C* __restrict__ amps, 
     const uint64_t pol = policy_evict_first();
     for (long long it = 0; it < mine; ++it) {
       const int s = int(it % S);
-      if (it >= S) mbar_wait(&empty[s], uint32_t(((it - S) / S) & 1));
+      if (it >= S) mbar_wait_sleep(&empty[s], uint32_t(((it - S) / S) & 1));
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
       __syncwarp();
