@@ -109,8 +109,8 @@ int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_be
                    int* flags);
 /* Register-phase encoding of kernel op i.  Dense: *mask = register-bit mask.
  * Diagonal: *mask = kt, src[0..kt) = thread bits of table bits kr..; src must
- * hold SVB_MAX_TARGETS + 2 ints, src[8..9] = the 64-bit map rho -> register
- * part of the table index (4 bits per rho). */
+ * hold 2 * SVB_MAX_TARGETS ints: src[8..15] viewed as 32 bytes map each rho
+ * to the register part of the table index. */
 int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
                       double* coeffs, int coeff_cap);
 int svb_plan_execute(svb_plan* plan, void* amps, void* stream);

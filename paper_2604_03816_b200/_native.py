@@ -144,14 +144,14 @@ class NativePlan:
                 "est_cost": info.est_cost, "reg_bits": info.reg_bits, "num_phases": info.num_phases}
 
     def phase(self, p: int, f: int) -> dict:
-        R = (C.c_int * 4)()
+        R = (C.c_int * 8)()
         b, e, fl = C.c_int(), C.c_int(), C.c_int()
         check(lib().svb_plan_phase(self._h, p, f, R, C.byref(b), C.byref(e), C.byref(fl)))
         return {"R": list(R), "op_begin": b.value, "op_end": e.value, "flags": fl.value}
 
     def phase_op(self, p: int, i: int) -> dict:
         kind, k, mask = C.c_int(), C.c_int(), C.c_int()
-        src = np.zeros(SVB_MAX_TARGETS + 2, dtype=np.int32)
+        src = np.zeros(2 * SVB_MAX_TARGETS, dtype=np.int32)
         co = np.zeros(2 * 4096, dtype=np.float64)
         n = check(lib().svb_plan_phase_op(self._h, p, i, C.byref(kind), C.byref(k), C.byref(mask),
                                           _iptr(src), _dptr(co), 4096))
@@ -159,7 +159,7 @@ class NativePlan:
                "coeffs": co[:2 * n].view(np.complex128).copy()}
         if kind.value == 1:
             out["thread_bits"] = [int(x) for x in src[:mask.value]]
-            out["rmap"] = int(np.uint32(src[8])) | (int(np.uint32(src[9])) << 32)
+            out["rmap"] = src[8:16].view(np.uint8).copy()
         return out
 
     def pass_gates(self, p: int) -> list[int]:

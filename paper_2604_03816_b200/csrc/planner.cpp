@@ -11,6 +11,7 @@ namespace svb {
 int default_tile_bits(int prec) { return prec == SVB_C64 ? 12 : 11; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
 int default_reg_bits(int prec) { return prec == SVB_C64 ? 4 : 3; }
+// tile = RB + 8 qubits for the register kernel
 
 namespace {
 
@@ -114,7 +115,7 @@ size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 // (diagonal ops fit any phase).  Ops are reordered into phase order.
 // Returns false when the pass must use the shared-memory kernel instead.
 bool build_phases(Pass& p, int RB, int prec) {
-  if (RB < 1 || RB > 4 || p.T != RB + 8) return false;
+  if (RB < 1 || RB > 5 || p.T != RB + 8) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
   for (const KernelOp& op : p.ops)
@@ -221,13 +222,11 @@ bool build_phases(Pass& p, int RB, int prec) {
         const int kr = int(regb.size()), kt = int(thrb.size());
         ro.mask = kt;  // stored in OpDesc.pad
         for (int j = 0; j < kt; ++j) ro.src[j] = thrb[j].first;
-        unsigned long long rmap = 0;
         for (int rho = 0; rho < (1 << RB); ++rho) {
           int d = 0;
           for (int j = 0; j < kr; ++j) d |= ((rho >> regb[j].first) & 1) << j;
-          rmap |= static_cast<unsigned long long>(d) << (4 * rho);
+          ro.rmap[rho] = static_cast<unsigned char>(d);
         }
-        ro.rmap = rmap;
         ro.coeff.assign(op.coeff.size(), cd());
         for (size_t nidx = 0; nidx < op.coeff.size(); ++nidx) {
           int old = 0;

@@ -36,7 +36,7 @@ struct KernelOp {
 
 // Register-phase encoding of a pass for k_reg_pass (see svb_regpass.cuh).
 struct RegPhase {
-  int R[4] = {0, 0, 0, 0};  // register bit i <-> tile-local bit R[i] (ascending)
+  int R[8] = {0};           // register bit i <-> tile-local bit R[i] (ascending)
   int op_begin = 0, op_end = 0;
   int flags = 0;
 };
@@ -45,7 +45,7 @@ struct RegOp {
   int k = 0;
   int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
   int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
-  unsigned long long rmap = 0;  // diagonal: 4-bit register part of the table index per rho
+  unsigned char rmap[32] = {0};  // diagonal: register part of the table index per rho
   std::vector<cd> coeff;   // dense: matrix permuted to ascending register bits
 };
 

@@ -44,6 +44,7 @@ bool valid_prec(int p) { return p == SVB_C64 || p == SVB_C128; }
 
 struct DeviceFacts {
   int sm_count = 0;
+  int max_smem = 0;
   int ctas_per_sm_c64 = 0;
   int ctas_per_sm_c128 = 0;
   bool attrs_set = false;
@@ -61,10 +62,12 @@ int device_facts(DeviceFacts** out) {
     SVB_CUDA(cudaDeviceGetAttribute(&f.sm_count, cudaDevAttrMultiProcessorCount, dev));
     int max_optin = 0;
     SVB_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    f.max_smem = max_optin;
     const void* fns[] = {(const void*)k_tile_pass<float2, 2>,  (const void*)k_tile_pass<float2, 3>,
                          (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
+                         (const void*)k_reg_pass<float2, 5>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -104,7 +107,7 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
       d.op_begin = p.phases[f].op_begin;
       d.op_end = p.phases[f].op_end;
       d.flags = p.phases[f].flags;
-      for (int i = 0; i < 4; ++i) d.R[i] = p.phases[f].R[i];
+      for (int i = 0; i < 8; ++i) d.R[i] = p.phases[f].R[i];
     }
     for (size_t i = 0; i < p.reg_ops.size(); ++i) {
       const RegOp& ro = p.reg_ops[i];
@@ -115,8 +118,7 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
       d.coeff_off = off;
       d.pad = ro.mask;
       if (ro.kind == OP_DIAG) {
-        d.tgt[0] = int(static_cast<unsigned>(ro.rmap & 0xffffffffull));
-        d.tgt[1] = int(static_cast<unsigned>(ro.rmap >> 32));
+        std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
       }
       for (const cd& z : ro.coeff) {
@@ -197,12 +199,19 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     // tensor map refused (should not happen for planned shapes): 1-D bulk copies
     a.h.tma_rank = 0;
   }
+  // deepest TMA ring that fits the opt-in shared memory (>= 2 stages)
+  while (a.h.stages > 2 && tile_pass_smem_bytes<C>(a.h) > size_t(f->max_smem)) --a.h.stages;
   const size_t smem = tile_pass_smem_bytes<C>(a.h);
   static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
   void (*fn)(C*, PassArgs<C>);
   if (a.h.n_phases > 0) {
-    fn = a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
-    if (a.h.reg_bits != 3 && a.h.reg_bits != 4) return fail(SVB_EUNSUPPORTED, "reg_bits must be 3 or 4");
+    if constexpr (sizeof(C) == 8) {
+      if (a.h.reg_bits < 3 || a.h.reg_bits > 5) return fail(SVB_EUNSUPPORTED, "c64 reg_bits must be 3..5");
+      fn = a.h.reg_bits == 5 ? k_reg_pass<C, 5> : a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
+    } else {
+      if (a.h.reg_bits < 3 || a.h.reg_bits > 4) return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4");
+      fn = a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
+    }
   } else {
     int kmax = 0;
     for (int i = 0; i < a.h.n_ops; ++i)
@@ -363,7 +372,7 @@ int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_be
   const Pass& p = plan->plan.passes[pass];
   if (phase < 0 || phase >= int(p.phases.size())) return fail(SVB_EINVAL, "phase index out of range");
   const RegPhase& ph = p.phases[phase];
-  for (int i = 0; i < 4; ++i) R[i] = ph.R[i];
+  for (int i = 0; i < 8; ++i) R[i] = ph.R[i];
   *op_begin = ph.op_begin;
   *op_end = ph.op_end;
   *flags = ph.flags;
@@ -381,10 +390,7 @@ int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, 
   *k = op.k;
   *mask = op.mask;
   for (int j = 0; j < kMaxK; ++j) src[j] = op.src[j];
-  if (op.kind == OP_DIAG) {  // src[8], src[9] carry the 64-bit register map
-    src[8] = int(static_cast<unsigned>(op.rmap & 0xffffffffull));
-    src[9] = int(static_cast<unsigned>(op.rmap >> 32));
-  }
+  if (op.kind == OP_DIAG) std::memcpy(src + kMaxK, op.rmap, sizeof(op.rmap));  // src[8..15]
   if (coeffs) {
     if (int(op.coeff.size()) > coeff_cap) return fail(SVB_EINVAL, "coefficient capacity too small");
     for (size_t e = 0; e < op.coeff.size(); ++e) {

@@ -21,11 +21,11 @@ template <class C>
 struct Swz;
 template <>
 struct Swz<float2> {  // 16 x 8 B per 128-B bank row
-  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 4) ^ (i >> 8)) & 15); }
+  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 4) ^ (i >> 8) ^ (i >> 12)) & 15); }
 };
 template <>
 struct Swz<double2> {  // 8 x 16 B per 128-B bank row
-  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7); }
+  static __device__ __forceinline__ int f(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7); }
 };
 
 template <int RB>
@@ -78,11 +78,9 @@ __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, cons
   for (int j = 0; j < kMaxK; ++j)
     if (j < kt) dt |= ((tid >> op.srt[j]) & 1) << j;
   dt <<= kr;
-  const unsigned long long rmap =
-      (static_cast<unsigned long long>(static_cast<unsigned>(op.tgt[1])) << 32) | static_cast<unsigned>(op.tgt[0]);
 #pragma unroll
   for (int rho = 0; rho < (1 << RB); ++rho) {
-    const int d = dt | int((rmap >> (4 * rho)) & 15);
+    const int d = dt | ((op.tgt[rho >> 2] >> (8 * (rho & 3))) & 0xff);
     v[rho] = cmul(v[rho], table[d]);
   }
 }
@@ -101,6 +99,8 @@ __device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, con
     break;
     SVB_CASE(1) SVB_CASE(2) SVB_CASE(3) SVB_CASE(4) SVB_CASE(5) SVB_CASE(6) SVB_CASE(7)
     SVB_CASE(8) SVB_CASE(9) SVB_CASE(10) SVB_CASE(11) SVB_CASE(12) SVB_CASE(13) SVB_CASE(14)
+    SVB_CASE(16) SVB_CASE(17) SVB_CASE(18) SVB_CASE(19) SVB_CASE(20) SVB_CASE(21) SVB_CASE(22)
+    SVB_CASE(24) SVB_CASE(25) SVB_CASE(26) SVB_CASE(28)
 #undef SVB_CASE
     default: break;
   }
@@ -169,7 +169,7 @@ struct GlobalAddr {
 };
 
 template <class C, int RB>
-__global__ void __launch_bounds__(kThreads, 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+__global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + 8;
   constexpr int NR = 1 << RB;
   extern __shared__ __align__(128) unsigned char smem[];

@@ -36,14 +36,15 @@ struct OpDesc {
 
 // Register-resident execution (k_reg_pass): a pass is a list of phases; in
 // phase p the register bits are R[0..RB) and ops [op_begin, op_end) act on
-// them (dense: OpDesc.pad = register-bit mask; diagonal: OpDesc.tgt[b] =
-// register index, or 16 + thread-bit index).
+// them (dense: OpDesc.pad = register-bit mask; diagonal: OpDesc.pad = kt,
+// OpDesc.srt[0..kt) = thread bits, OpDesc.tgt viewed as 32 bytes = the
+// register part of the table index for each rho).
 constexpr int kMaxPhases = 32;
 enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2 };
 
 struct PhaseDesc {
   int op_begin, op_end, flags, pad;
-  int R[4];
+  int R[8];
 };
 
 struct PassHeader {

@@ -86,7 +86,8 @@ def test_golden_fused_circuits(eng, golden_fused, prec):
 
 OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits": 1, "cost_budget": -1.0},
         {"no_diag_merge": 1, "stages": 2}, {"stages": 4, "max_ops_per_pass": 1},
-        {"no_reg_phases": 1}, {"reg_bits": 3, "tile_bits": 11}, {"cost_budget": -1.0, "stages": 2}]
+        {"no_reg_phases": 1}, {"reg_bits": 3, "tile_bits": 11}, {"cost_budget": -1.0, "stages": 2},
+        {"reg_bits": 5, "tile_bits": 13, "cost_budget": 3.0}]
 
 
 @pytest.mark.parametrize("opts", OPTS, ids=[str(o) for o in OPTS])

@@ -202,7 +202,7 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                             dt |= ((tid >> tb) & 1) << (kr + j)
                         tab = op["coeffs"].astype(v.dtype)
                         for rho in range(nr):
-                            v[:, rho] *= tab[dt | ((op["rmap"] >> (4 * rho)) & 15)]
+                            v[:, rho] *= tab[dt | int(op["rmap"][rho])]
                 buf[loc] = v
             amps[idx] = buf
     return amps
@@ -226,3 +226,17 @@ def test_register_phase_encoding(name, make, prec):
     assert all(i["reg_bits"] > 0 and i["num_phases"] >= 1 for i in infos), infos
     got = emulate_reg(plan, c.num_qubits, prec)
     assert np.abs(got - want).max() <= (1e-12 if prec == "double" else 1e-5)
+
+
+@pytest.mark.parametrize("prec,rb", [("single", 5), ("single", 3), ("double", 4)])
+def test_register_phase_encoding_other_widths(prec, rb):
+    c = fuse(gen.layered_circuit(14, layers=5, seed=6), 2)[0]
+    q = fuse(gen.qft_circuit(13), 2)[0]
+    for circ in (c, q):
+        want = orc.run_circuit(circ, "double")
+        plan = CircuitPlan(circ.num_qubits, Precision(prec), circ.gates,
+                           plan_options(reg_bits=rb, tile_bits=rb + 8))
+        infos = plan.passes()
+        assert all(i["reg_bits"] == rb for i in infos)
+        got = emulate_reg(plan, circ.num_qubits, prec)
+        assert np.abs(got - want).max() <= (1e-12 if prec == "double" else 1e-5)
