@@ -115,7 +115,8 @@ size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 // (diagonal ops fit any phase).  Ops are reordered into phase order.
 // Returns false when the pass must use the shared-memory kernel instead.
 bool build_phases(Pass& p, int RB, int prec) {
-  if (RB < 1 || RB > 5 || p.T != RB + 8) return false;
+  // instantiated register kernels: c64 RB 3..5, c128 RB 3..4
+  if (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4) || p.T != RB + 8) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
   for (const KernelOp& op : p.ops)

@@ -78,7 +78,7 @@ int device_facts(DeviceFacts** out) {
 }
 
 template <class C>
-void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
+void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) {
   std::memset(&a.h, 0, sizeof(a.h));
   a.h.T = p.T;
   a.h.L = p.L;
@@ -96,6 +96,27 @@ void fill_args(const Pass& p, int stages, PassArgs<C>& a) {
     a.h.tma_box[d] = p.tma_box[d];
   }
   a.h.word_shift = sizeof(C) == 16 ? 1 : 0;
+  {  // runs of non-tile bits (ascending), consumed from the tile index low bits up
+    std::vector<char> in_tile(64, 0);
+    for (int q = 0; q < p.L; ++q) in_tile[q] = 1;
+    for (int b = 0; b < p.m; ++b) in_tile[p.high[b]] = 1;
+    int src = 0, nr = 0;
+    for (int q = 0; q < n_local_for_args;) {
+      if (in_tile[q]) {
+        ++q;
+        continue;
+      }
+      int len = 0;
+      while (q + len < n_local_for_args && !in_tile[q + len]) ++len;
+      a.h.gap_src[nr] = src;
+      a.h.gap_dst[nr] = q;
+      a.h.gap_len[nr] = len;
+      ++nr;
+      src += len;
+      q += len;
+    }
+    a.h.n_gap_runs = nr;
+  }
   a.h.stages = stages;
   a.h.n_phases = int(p.phases.size());
   a.h.reg_bits = p.reg_bits;
@@ -330,13 +351,13 @@ int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int
   if (prec == SVB_C64) {
     p->args64.resize(np);
     for (int i = 0; i < np; ++i) {
-      fill_args<float2>(p->plan.passes[i], p->stages, p->args64[i]);
+      fill_args<float2>(p->plan.passes[i], p->stages, n_local, p->args64[i]);
       p->args64[i].h.n_tiles = n_tiles;
     }
   } else {
     p->args128.resize(np);
     for (int i = 0; i < np; ++i) {
-      fill_args<double2>(p->plan.passes[i], p->stages, p->args128[i]);
+      fill_args<double2>(p->plan.passes[i], p->stages, n_local, p->args128[i]);
       p->args128[i].h.n_tiles = n_tiles;
     }
   }

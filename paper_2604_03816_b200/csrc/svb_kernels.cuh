@@ -52,7 +52,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // not steal issue slots from the compute warps sharing its scheduler.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) __nanosleep(200);
+  while (!mbar_try_wait(a, parity)) __nanosleep(800);
 }
 __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
                                           uint64_t policy) {
@@ -236,11 +236,9 @@ __device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* po
 }
 
 __device__ __forceinline__ long long tile_base(long long tile, const PassHeader& h) {
-  long long g = tile << h.L;
-  for (int b = 0; b < h.m; ++b) {
-    const int p = h.high_sorted[b];
-    g = ((g >> p) << (p + 1)) | (g & ((1LL << p) - 1));
-  }
+  long long g = 0;
+  for (int r = 0; r < h.n_gap_runs; ++r)
+    g |= ((tile >> h.gap_src[r]) & ((1LL << h.gap_len[r]) - 1)) << h.gap_dst[r];
   return g;
 }
 __device__ __forceinline__ long long chunk_offset(int c, const PassHeader& h) {

@@ -252,6 +252,15 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
   lin_g.gthr = global_of(tid, h);
 #pragma unroll
   for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(8 + i, h);
+  // global addressing of the last phase's direct store is tile-invariant
+  GlobalAddr<RB> last_g;
+  {
+    const PhaseDesc& lp = args.phases[np - 1];
+    const PhaseAddr<C, RB> la(lp, tid);
+    last_g.gthr = global_of(la.base, h);
+#pragma unroll
+    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.R[i], h);
+  }
   int s = 0;
   uint32_t parity = 0;
   for (long long it = 0; it < mine; ++it, (++s == S ? (s = 0, parity ^= 1) : 0)) {
@@ -293,13 +302,9 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
       } else if (!tout) {
         // direct store from registers (coalesced: R avoids the bank-row bits)
-        GlobalAddr<RB> ga;
-        ga.gthr = global_of(a.base, h);
+        C* __restrict__ dst = amps + tile_base(tile, h) + last_g.gthr;
 #pragma unroll
-        for (int i = 0; i < RB; ++i) ga.goff[i] = 1LL << gpos(ph.R[i], h);
-        C* __restrict__ dst = amps + tile_base(tile, h);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) dst[ga.at(r)] = v[r];
+        for (int r = 0; r < NR; ++r) dst[last_g.at(r) - last_g.gthr] = v[r];
       } else {
         // swizzled smem, then contiguous reads -> coalesced global stores
 #pragma unroll

@@ -62,6 +62,10 @@ struct PassHeader {
   int tma_bits[5];
   int tma_box[5];     // log2 box extent (0 = box 1)
   int word_shift;     // 0 for c64 (one 8-B word per amplitude), 1 for c128
+  // tile index -> shard offset of the tile origin: the tile index bits fill
+  // the non-tile bits in runs: origin = sum ((tile >> src) & (2^len-1)) << dst
+  int n_gap_runs;
+  int gap_src[kMaxHigh + 1], gap_dst[kMaxHigh + 1], gap_len[kMaxHigh + 1];
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)
