@@ -129,6 +129,15 @@ int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream);
 int svb_probabilities(const void* amps, int prec, long long offset, long long count,
                       double* out_device, void* stream);
 
+/* Measurement sampling on the device -- replaces the host path of sample /
+ * sample_from_probabilities (ref engines.py:307-337): per-block FP64 sums of
+ * |amp|^2 (blocks of 2^log_block amplitudes), then for each target x (= the
+ * host's Philox draw times the total) the index numpy.searchsorted(cdf, x,
+ * side="right") would return, given the inclusive block prefix sums. */
+int svb_block_sums(const void* amps, int n_local, int prec, int log_block, double* out_device, void* stream);
+int svb_sample_search(const void* amps, int n_local, int prec, int log_block, const double* block_cum,
+                      const double* targets, long long shots, long long* out_indices, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

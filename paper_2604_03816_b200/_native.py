@@ -25,7 +25,7 @@ EXPORTS = (
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
     "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
-    "svb_probabilities",
+    "svb_probabilities", "svb_block_sums", "svb_sample_search",
 )
 
 
@@ -82,6 +82,8 @@ def lib():
         "svb_dot": (i, [vp, vp, i, i, dp, vp]),
         "svb_norm2": (i, [vp, i, i, dp, vp]),
         "svb_probabilities": (i, [vp, i, ll, ll, vp, vp]),
+        "svb_block_sums": (i, [vp, i, i, i, vp, vp]),
+        "svb_sample_search": (i, [vp, i, i, i, vp, vp, ll, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

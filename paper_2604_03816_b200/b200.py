@@ -269,6 +269,40 @@ class B200Engine(EngineBase):
             ov /= self.norm_squared(a) * self.norm_squared(b)
         return float(ov)
 
+    def sample(self, state: DeviceStateVector, shots: int, seed: int):
+        """shots draws from |amp|^2 with the reference's semantics (ref
+        engines.py:307-337): Philox(key=seed) uniforms scaled by the total,
+        inverse CDF (searchsorted side='right'), qubit 0 rightmost.  The CDF
+        never leaves the device; only the draws and the indices cross PCIe."""
+        from .engines import SampleResult
+        if shots < 0:
+            raise ValueError("shots must be >= 0")
+        if shots == 0:
+            return SampleResult({}, 0)
+        n = state.num_qubits
+        lb = min(n, 12)
+        nb = 1 << (n - lb)
+        dev = state.tensor.device
+        sums = torch.empty(nb, dtype=torch.float64, device=dev)
+        pc = prec_code(state.precision)
+        s = C.c_void_p(self.stream())
+        _native.check(_native.lib().svb_block_sums(C.c_void_p(state.tensor.data_ptr()), n, pc, lb,
+                                                   C.c_void_p(sums.data_ptr()), s))
+        cum = torch.cumsum(sums, 0)
+        total = float(cum[-1].item())
+        if abs(total - 1.0) > 1e-4:
+            raise ValueError(f"state norm deviates from 1 by {abs(total - 1.0):.2e}; "
+                             "refusing to sample from a corrupted state")
+        draws = np.random.Generator(np.random.Philox(key=seed)).random(shots)
+        x = torch.from_numpy(draws * total).to(dev)
+        idx = torch.empty(shots, dtype=torch.int64, device=dev)
+        _native.check(_native.lib().svb_sample_search(
+            C.c_void_p(state.tensor.data_ptr()), n, pc, lb, C.c_void_p(cum.data_ptr()),
+            C.c_void_p(x.data_ptr()), shots, C.c_void_p(idx.data_ptr()), s))
+        host = np.minimum(idx.cpu().numpy(), (1 << n) - 1)
+        values, counts = np.unique(host, return_counts=True)
+        return SampleResult({format(int(v), f"0{n}b"): int(c) for v, c in zip(values, counts)}, shots)
+
     def probabilities(self, state: DeviceStateVector) -> np.ndarray:
         out = torch.empty(1 << state.num_qubits, dtype=torch.float64, device=state.tensor.device)
         _native.check(_native.lib().svb_probabilities(

@@ -399,7 +399,8 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   }
   svb_plan_options opt = opt_in;
   int T = opt.tile_bits > 0 ? opt.tile_bits : default_tile_bits(prec);
-  if (T > 13) T = 13;
+  // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)
+  if (T > (prec == SVB_C64 ? 13 : 12)) T = prec == SVB_C64 ? 13 : 12;
   if (T > n) T = n;
   int Lmin = opt.min_low_bits > 0 ? opt.min_low_bits : default_min_low_bits(prec);
   if (Lmin > T) Lmin = T;

@@ -502,6 +502,43 @@ int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream) {
   return SVB_OK;
 }
 
+int svb_block_sums(const void* amps, int n_local, int prec, int log_block, double* out_device, void* stream) {
+  if (!amps || !out_device) return fail(SVB_EINVAL, "null argument");
+  if (!valid_prec(prec) || log_block < 0 || log_block > n_local || n_local > 62)
+    return fail(SVB_EINVAL, "bad shape");
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long nb = 1LL << (n_local - log_block);
+  const unsigned grid = unsigned(std::min<long long>(nb, (long long)f->sm_count * 8));
+  if (prec == SVB_C64)
+    k_block_sums<float2><<<grid, 256, 0, s>>>(static_cast<const float2*>(amps), nb, log_block, out_device);
+  else
+    k_block_sums<double2><<<grid, 256, 0, s>>>(static_cast<const double2*>(amps), nb, log_block, out_device);
+  SVB_CUDA(cudaGetLastError());
+  return SVB_OK;
+}
+
+int svb_sample_search(const void* amps, int n_local, int prec, int log_block, const double* block_cum,
+                      const double* targets, long long shots, long long* out_indices, void* stream) {
+  if (!amps || !block_cum || !targets || !out_indices || shots < 0) return fail(SVB_EINVAL, "bad argument");
+  if (!valid_prec(prec) || log_block < 0 || log_block > n_local || n_local > 62)
+    return fail(SVB_EINVAL, "bad shape");
+  if (shots == 0) return SVB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long nb = 1LL << (n_local - log_block);
+  const unsigned grid = unsigned((shots + 255) / 256);
+  if (prec == SVB_C64)
+    k_sample_search<float2><<<grid, 256, 0, s>>>(static_cast<const float2*>(amps), nb, log_block, block_cum,
+                                                 targets, shots, out_indices);
+  else
+    k_sample_search<double2><<<grid, 256, 0, s>>>(static_cast<const double2*>(amps), nb, log_block, block_cum,
+                                                  targets, shots, out_indices);
+  SVB_CUDA(cudaGetLastError());
+  return SVB_OK;
+}
+
 int svb_probabilities(const void* amps, int prec, long long offset, long long count, double* out_device,
                       void* stream) {
   if (!amps || !out_device || offset < 0 || count < 0) return fail(SVB_EINVAL, "bad argument");

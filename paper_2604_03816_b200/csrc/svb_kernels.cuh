@@ -380,6 +380,62 @@ __global__ void k_dot(const C* __restrict__ a, const C* __restrict__ b, long lon
   }
 }
 
+// Sum of |amp|^2 (FP64) over each block of 2^lb amplitudes; one CTA per block.
+template <class C>
+__global__ void k_block_sums(const C* __restrict__ a, long long n_blocks, int lb, double* __restrict__ out) {
+  __shared__ double red[32];
+  for (long long b = blockIdx.x; b < n_blocks; b += gridDim.x) {
+    const C* p = a + (b << lb);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (1 << lb); i += blockDim.x) {
+      const double r = p[i].x, m = p[i].y;
+      acc += r * r + m * m;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) out[b] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// Inverse-CDF search (numpy searchsorted side='right' on the cumulative
+// |amp|^2): block by binary search over the inclusive block prefix, then a
+// sequential scan inside the block.  One thread per draw.
+template <class C>
+__global__ void k_sample_search(const C* __restrict__ a, long long n_blocks, int lb,
+                                const double* __restrict__ block_cum, const double* __restrict__ x,
+                                long long shots, long long* __restrict__ out) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= shots) return;
+  const double t = x[s];
+  long long lo = 0, hi = n_blocks;  // first block with block_cum > t
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (block_cum[mid] > t) hi = mid; else lo = mid + 1;
+  }
+  if (lo >= n_blocks) {
+    out[s] = (n_blocks << lb) - 1;
+    return;
+  }
+  double cum = lo > 0 ? block_cum[lo - 1] : 0.0;
+  const C* p = a + (lo << lb);
+  long long idx = (lo << lb) + (1 << lb) - 1;
+  for (int i = 0; i < (1 << lb); ++i) {
+    const double r = p[i].x, m = p[i].y;
+    cum += r * r + m * m;
+    if (cum > t) {
+      idx = (lo << lb) + i;
+      break;
+    }
+  }
+  out[s] = idx;
+}
+
 template <class C>
 __global__ void k_probabilities(const C* __restrict__ a, long long n, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {

@@ -40,6 +40,14 @@ else:
                              f"capacity {capacity_bytes}")
 
 
+@dataclass
+class SampleResult:
+    """Measurement counts keyed by bitstring, qubit 0 rightmost (ref engines.py:52-57)."""
+
+    counts: dict
+    shots: int
+
+
 @dataclass(frozen=True)
 class EngineId:
     name: str

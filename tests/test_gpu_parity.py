@@ -199,3 +199,56 @@ def test_engine_api_contract():
     e.apply_gate(s, GateOp(GateKind.X, (0,)))
     assert s.amplitudes[4] == 1
     e.release(s)
+
+
+def test_device_sampling_matches_reference_semantics(eng):
+    """sample() keeps ref engines.py:307-337 semantics: same counts as the
+    numpy inverse-CDF path on the same probabilities and Philox seed."""
+    def ref_sample(amps, shots, seed, n):
+        probs = np.abs(amps.astype(np.complex128)) ** 2
+        cdf = np.cumsum(probs)
+        draws = np.random.Generator(np.random.Philox(key=seed)).random(shots)
+        idx = np.minimum(np.searchsorted(cdf, draws * cdf[-1], side="right"), len(cdf) - 1)
+        v, c = np.unique(idx, return_counts=True)
+        return {format(int(a), f"0{n}b"): int(b) for a, b in zip(v, c)}
+    for n, circ in ((4, gen.ghz_circuit(4)), (10, fuse(gen.layered_circuit(10, layers=3), 2)[0]),
+                    (14, gen.qft_circuit(14))):
+        for prec in (Precision.DOUBLE, Precision.SINGLE):
+            s = eng.run_circuit(circ, prec)
+            got = eng.sample(s, 4096, seed=11)
+            assert got.shots == 4096 and sum(got.counts.values()) == 4096
+            assert got.counts == ref_sample(s.amplitudes, 4096, 11, n)
+    s = eng.run_circuit(gen.ghz_circuit(4), Precision.DOUBLE)
+    assert eng.sample(s, 0, seed=1).counts == {}
+
+
+def test_layered33_c128_mirror_full_size(eng):
+    """BASELINE config 4 at full size (33 q, complex128, 128 GiB state): the
+    fused layered circuit followed by its inverse returns |0...0>."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < (1 << 37) + (8 << 30):
+        pytest.skip("needs ~136 GiB free device memory")
+    f, rep = fuse(gen.layered_circuit(33), 2)
+    assert rep.fused_gate_count == 224
+    mirror = Circuit(33, list(f.gates) + list(_dagger(f).gates))
+    s = eng.run_circuit(mirror, Precision.DOUBLE)
+    a0 = complex(s.tensor[0].item())
+    assert abs(a0 - 1.0) <= 1e-10, a0
+    assert abs(eng.norm_squared(s) - 1.0) <= 1e-10
+    eng.release(s)
+    del s
+    torch.cuda.empty_cache()
+
+
+def test_reference_registry_dropin():
+    """With the reference package importable, ``aqsim.run_circuit("b200")`` runs
+    on the device and matches the reference engine (skipped on the GPU box,
+    where /root/reference is absent)."""
+    aqsim = pytest.importorskip("aqsim")
+    import paper_2604_03816_b200  # noqa: F401  (registers "b200")
+    c = aqsim.qft_circuit(8)
+    got = aqsim.run_circuit("b200", c, aqsim.Precision.DOUBLE)
+    want = aqsim.run_circuit("reference", c, aqsim.Precision.DOUBLE)
+    assert np.abs(got.amplitudes - want.amplitudes).max() <= 1e-12
+    assert aqsim.state_fidelity(got, want) == pytest.approx(1.0, abs=1e-10)
