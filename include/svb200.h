@@ -49,14 +49,14 @@ typedef struct svb_plan svb_plan;
 
 /* Planner knobs; zero-initialise for defaults. */
 typedef struct svb_plan_options {
-  int tile_bits;        /* qubits per shared-memory tile (0: 12 for c64, 11 for c128) */
+  int tile_bits;        /* qubits per shared-memory tile (0: 13 for c64, 11 for c128) */
   int min_low_bits;     /* contiguous low qubits always in the tile (0: 512-B chunks) */
   int max_ops_per_pass; /* 0: 48 (kernel limit)                                      */
-  double cost_budget;   /* compute budget per pass as a multiple of the pass's HBM
-                           time; 0: default 1.0, <0: unlimited                       */
+  double cost_budget;   /* modelled compute per pass as a multiple of the pass's HBM
+                           time; 0: default (3.0 c64, 2.0 c128), <0: unlimited       */
   int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
   int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
-  int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 4 for c64, 3 c128) */
+  int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
 } svb_plan_options;
 

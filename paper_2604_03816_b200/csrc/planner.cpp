@@ -8,9 +8,13 @@
 
 namespace svb {
 
-int default_tile_bits(int prec) { return prec == SVB_C64 ? 12 : 11; }
+// Measured on B200 (profiles/r01_*): c64 passes are FFMA-issue bound, so the
+// widest register tile (13 qubits, 32 amplitudes per thread) wins; c128 uses
+// 11-qubit tiles with 8 amplitudes per thread (FP64 register pressure).
+int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 11; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
-int default_reg_bits(int prec) { return prec == SVB_C64 ? 4 : 3; }
+int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 3; }
+double default_cost_budget(int prec) { return prec == SVB_C64 ? 3.0 : 2.0; }
 // tile = RB + 8 qubits for the register kernel
 
 namespace {
@@ -409,7 +413,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   const int mmax = T - Lmin;
   const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
                           ? opt.max_ops_per_pass : kMaxOps;
-  const double budget = opt.cost_budget == 0.0 ? 1.0 : opt.cost_budget;
+  const double budget = opt.cost_budget == 0.0 ? default_cost_budget(prec) : opt.cost_budget;
   const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
   const CostModel cm(prec);
 
@@ -578,7 +582,8 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     }
     p.ops = std::move(ops);
     p.num_gates = int(taken.size());
-    const int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
+    int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
+    if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile
     if (!opt.no_reg_phases && !build_phases(p, RB, prec)) {
       p.phases.clear();
       p.reg_ops.clear();

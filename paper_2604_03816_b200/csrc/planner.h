@@ -79,6 +79,7 @@ struct Plan {
 int default_tile_bits(int prec);
 int default_min_low_bits(int prec);
 int default_reg_bits(int prec);
+double default_cost_budget(int prec);
 
 // Parse + classify the raw ABI arrays into gates (diagonal detection).
 bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const double* op_mats,
