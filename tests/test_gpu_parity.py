@@ -252,3 +252,15 @@ def test_reference_registry_dropin():
     want = aqsim.run_circuit("reference", c, aqsim.Precision.DOUBLE)
     assert np.abs(got.amplitudes - want.amplitudes).max() <= 1e-12
     assert aqsim.state_fidelity(got, want) == pytest.approx(1.0, abs=1e-10)
+
+
+def test_cli_run_and_bench_scaling(capsys):
+    import json as _json
+    from paper_2604_03816_b200.__main__ import main
+    assert main(["run", "ghz-5", "--shots", "1000", "--seed", "3", "--no-timing"]) == 0
+    rep = _json.loads(capsys.readouterr().out)
+    assert rep["engine_chosen"] == "b200" and rep["g_fused"] >= 1
+    assert set(rep["counts"]) == {"00000", "11111"} and sum(rep["counts"].values()) == 1000
+    assert main(["bench-scaling", "--qubits", "10,12", "--repetitions", "1", "--no-timing"]) == 0
+    rows = _json.loads(capsys.readouterr().out)
+    assert [r["n"] for r in rows] == [10, 12]
