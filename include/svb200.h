@@ -58,6 +58,11 @@ typedef struct svb_plan_options {
   int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
   int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
+  int tensor_cores;     /* c64 only: 1 = fuse register phases into tcgen05 TF32x3
+                           GEMMs (k_tc_pass, 12-qubit tiles, 32 amps x 128 threads);
+                           0 = default (on for c64), -1 = off                      */
+  int tc_min_dense;     /* dense gates a phase needs to become a GEMM (0: 2)         */
+  int no_window_search; /* 1: plain program-order greedy pass building             */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */
@@ -71,6 +76,7 @@ typedef struct svb_pass_info {
   double est_cost;      /* planner cost estimate (fraction of HBM time) */
   int reg_bits;         /* > 0: register-phase kernel with 2^reg_bits amps per thread */
   int num_phases;       /* register phases (0 for the shared-memory kernel) */
+  int num_tc;           /* phases executed as tensor-core GEMMs */
 } svb_pass_info;
 
 int svb_abi_version(void);
@@ -104,9 +110,15 @@ int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap);
  * coefficients as complex128 (dense 4^k, diagonal 2^k entries). */
 int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* tile_targets,
                        double* coeffs, int coeff_cap);
-/* Register phase `phase` of pass `pass`: R[4] register bits, op range, flags. */
+/* Register phase `phase` of pass `pass`: R[8] register bits, op range, flags;
+ * op_mid / tc describe a tensor-core GEMM between ops [op_begin, op_mid) and
+ * [op_mid, op_end) (tc = -1: none). */
 int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_begin, int* op_end,
                    int* flags);
+int svb_plan_phase_tc(const svb_plan* plan, int pass, int phase, int* op_mid, int* tc);
+/* Fused GEMM matrix `tc` of pass `pass` (2^reg_bits x 2^reg_bits complex128,
+ * row-major, register-bit order) for tests. */
+int svb_plan_tc_matrix(const svb_plan* plan, int pass, int tc, double* out, int cap);
 /* Register-phase encoding of kernel op i.  Dense: *mask = register-bit mask.
  * Diagonal: *mask = kt, src[0..kt) = thread bits of table bits kr..; src must
  * hold 2 * SVB_MAX_TARGETS ints: src[8..15] viewed as 32 bytes map each rho

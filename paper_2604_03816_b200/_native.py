@@ -23,6 +23,7 @@ EXPORTS = (
     "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
     "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
+    "svb_plan_phase_tc", "svb_plan_tc_matrix",
     "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
     "svb_probabilities", "svb_block_sums", "svb_sample_search",
@@ -33,13 +34,15 @@ class PlanOptions(C.Structure):
     _fields_ = [("tile_bits", C.c_int), ("min_low_bits", C.c_int),
                 ("max_ops_per_pass", C.c_int), ("cost_budget", C.c_double),
                 ("no_diag_merge", C.c_int), ("stages", C.c_int), ("reg_bits", C.c_int),
-                ("no_reg_phases", C.c_int)]
+                ("no_reg_phases", C.c_int), ("tensor_cores", C.c_int), ("tc_min_dense", C.c_int),
+                ("no_window_search", C.c_int)]
 
 
 class PassInfo(C.Structure):
     _fields_ = [("tile_bits", C.c_int), ("low_bits", C.c_int), ("num_high", C.c_int),
                 ("high", C.c_int * 8), ("num_kernel_ops", C.c_int), ("num_gates", C.c_int),
-                ("est_cost", C.c_double), ("reg_bits", C.c_int), ("num_phases", C.c_int)]
+                ("est_cost", C.c_double), ("reg_bits", C.c_int), ("num_phases", C.c_int),
+                ("num_tc", C.c_int)]
 
 
 class NativeError(RuntimeError):
@@ -76,6 +79,8 @@ def lib():
         "svb_plan_kernel_op": (i, [vp, i, i, ip, ip, ip, dp, i]),
         "svb_plan_phase": (i, [vp, i, i, ip, ip, ip, ip]),
         "svb_plan_phase_op": (i, [vp, i, i, ip, ip, ip, ip, dp, i]),
+        "svb_plan_phase_tc": (i, [vp, i, i, ip, ip]),
+        "svb_plan_tc_matrix": (i, [vp, i, i, dp, i]),
         "svb_plan_execute": (i, [vp, vp, vp]),
         "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
         "svb_plan_destroy": (None, [vp]),
@@ -143,13 +148,23 @@ class NativePlan:
         return {"tile_bits": info.tile_bits, "low_bits": info.low_bits,
                 "high": [info.high[b] for b in range(info.num_high)],
                 "num_kernel_ops": info.num_kernel_ops, "num_gates": info.num_gates,
-                "est_cost": info.est_cost, "reg_bits": info.reg_bits, "num_phases": info.num_phases}
+                "est_cost": info.est_cost, "reg_bits": info.reg_bits, "num_phases": info.num_phases,
+                "num_tc": info.num_tc}
 
     def phase(self, p: int, f: int) -> dict:
         R = (C.c_int * 8)()
         b, e, fl = C.c_int(), C.c_int(), C.c_int()
         check(lib().svb_plan_phase(self._h, p, f, R, C.byref(b), C.byref(e), C.byref(fl)))
-        return {"R": list(R), "op_begin": b.value, "op_end": e.value, "flags": fl.value}
+        mid, tc = C.c_int(), C.c_int()
+        check(lib().svb_plan_phase_tc(self._h, p, f, C.byref(mid), C.byref(tc)))
+        return {"R": list(R), "op_begin": b.value, "op_end": e.value, "flags": fl.value,
+                "op_mid": mid.value, "tc": tc.value}
+
+    def tc_matrix(self, p: int, tc: int) -> np.ndarray:
+        out = np.zeros(2 * 1024, dtype=np.float64)
+        n = check(lib().svb_plan_tc_matrix(self._h, p, tc, _dptr(out), 1024))
+        d = int(round(n ** 0.5))
+        return out[:2 * n].view(np.complex128).reshape(d, d).copy()
 
     def phase_op(self, p: int, i: int) -> dict:
         kind, k, mask = C.c_int(), C.c_int(), C.c_int()

@@ -11,6 +11,10 @@ namespace svb {
 // Measured on B200 (profiles/r01_*): c64 passes are FFMA-issue bound, so the
 // widest register tile (13 qubits, 32 amplitudes per thread) wins; c128 uses
 // 11-qubit tiles with 8 amplitudes per thread (FP64 register pressure).
+constexpr int kMaxTcPerPass = 2;        // fused GEMM matrices per pass (shared memory)
+constexpr double kTcDenseCost = 0.15;   // planner cost of a dense gate in a tensor-core pass
+constexpr double kTcDefaultBudget = 3.0;
+
 int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 11; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
 int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 3; }
@@ -26,14 +30,17 @@ namespace {
 // the summed op cost stays below 1.0 (the default budget).
 struct CostModel {
   double s, fma, mem;
-  explicit CostModel(int prec) {
+  bool tc;
+  explicit CostModel(int prec, bool tensor = false) {
     s = prec == SVB_C64 ? 8.0 : 16.0;
     fma = prec == SVB_C64 ? 128.0 : 64.0;
     mem = 2.0 * s / 23.0;
+    tc = tensor;
   }
   // register-resident ops: FMAs plus, amortised, half a shared-memory
   // transpose per dense op (phases hold ~2 dense ops)
   double dense(int k) const {
+    if (tc) return kTcDenseCost;  // amortised share of a fused tensor-core phase
     double flops = 4.0 * double(1 << k) / fma;
     double smem = 0.5 * 2.0 * s / 128.0;
     return (flops * 1.2 + smem) / mem;
@@ -118,9 +125,12 @@ size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 // are already scheduled and whose bits fit the phase's RB register bits
 // (diagonal ops fit any phase).  Ops are reordered into phase order.
 // Returns false when the pass must use the shared-memory kernel instead.
-bool build_phases(Pass& p, int RB, int prec) {
-  // instantiated register kernels: c64 RB 3..5, c128 RB 3..4
-  if (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4) || p.T != RB + 8) return false;
+bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
+  // instantiated register kernels: c64 RB 3..5, c128 RB 3..4 (8 thread bits);
+  // the tensor-core kernel: c64 RB 5 with 7 thread bits
+  if (TB == 8 && (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4))) return false;
+  if (TB == 7 && (RB != 5 || prec != SVB_C64)) return false;
+  if (p.T != RB + TB) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
   for (const KernelOp& op : p.ops)
@@ -190,6 +200,7 @@ bool build_phases(Pass& p, int RB, int prec) {
       if (std::find(R.begin(), R.end(), b) == R.end()) R.push_back(b);
     std::sort(R.begin(), R.end());
     RegPhase rp;
+    rp.op_mid = ranges[ph].second;
     for (int i = 0; i < RB; ++i) rp.R[i] = R[i];
     rp.op_begin = ranges[ph].first;
     rp.op_end = ranges[ph].second;
@@ -266,7 +277,109 @@ bool build_phases(Pass& p, int RB, int prec) {
     p.phases.push_back(rp);
   }
   p.reg_bits = RB;
+  p.thread_bits = TB;
   return true;
+}
+
+// Expand a phase op (register encoding) to a 2^RB x 2^RB matrix.
+std::vector<cd> reg_op_matrix(const RegOp& ro, int RB) {
+  const int D = 1 << RB;
+  std::vector<cd> m(size_t(D) * D, cd());
+  if (ro.kind == OP_DIAG) {
+    for (int r = 0; r < D; ++r) m[size_t(r) * D + r] = ro.coeff[ro.rmap[r]];
+    return m;
+  }
+  std::vector<int> pos;
+  for (int i = 0; i < RB; ++i)
+    if ((ro.mask >> i) & 1) pos.push_back(i);
+  const int k = int(pos.size()), d = 1 << k;
+  for (int ro_ = 0; ro_ < D; ++ro_)
+    for (int ri = 0; ri < D; ++ri) {
+      if ((ro_ & ~ro.mask) != (ri & ~ro.mask)) continue;
+      int a = 0, b = 0;
+      for (int j = 0; j < k; ++j) {
+        a |= ((ro_ >> pos[j]) & 1) << j;
+        b |= ((ri >> pos[j]) & 1) << j;
+      }
+      m[size_t(ro_) * D + ri] = ro.coeff[size_t(a) * d + b];
+    }
+  return m;
+}
+
+// Fold, in up to max_tc phases, the longest run of register-only ops (dense
+// ops, and diagonal ops without thread-sourced bits) with >= min_dense dense
+// ops into one matrix product executed as a tensor-core GEMM (k_tc_pass).
+void fuse_tc_phases(Pass& p, int min_dense, int max_tc) {
+  const int RB = p.reg_bits;
+  const int D = 1 << RB;
+  struct Cand { int dense, phase, a, c; };
+  std::vector<Cand> cands;
+  for (int f = 0; f < int(p.phases.size()); ++f) {
+    const RegPhase& ph = p.phases[f];
+    int best = -1, ba = 0, bc = 0;
+    for (int a = ph.op_begin; a < ph.op_end;) {
+      int c = a, dense = 0;
+      while (c < ph.op_end && (p.reg_ops[c].kind == OP_DENSE || p.reg_ops[c].mask == 0)) {
+        dense += p.reg_ops[c].kind == OP_DENSE;
+        ++c;
+      }
+      if (c > a && dense > best) {
+        best = dense;
+        ba = a;
+        bc = c;
+      }
+      a = c > a ? c : a + 1;
+    }
+    if (best >= min_dense) cands.push_back({best, f, ba, bc});
+  }
+  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {
+    return x.dense != y.dense ? x.dense > y.dense : x.phase < y.phase;
+  });
+  if (int(cands.size()) > max_tc) cands.resize(max_tc);
+  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) { return x.phase < y.phase; });
+  std::vector<KernelOp> ops;
+  std::vector<RegOp> rops;
+  size_t ci = 0;
+  p.tc_mats.clear();
+  for (int f = 0; f < int(p.phases.size()); ++f) {
+    RegPhase& ph = p.phases[f];
+    const int b = ph.op_begin, e = ph.op_end;
+    const bool fuse = ci < cands.size() && cands[ci].phase == f;
+    const int a = fuse ? cands[ci].a : e, c = fuse ? cands[ci].c : e;
+    ph.op_begin = int(ops.size());
+    for (int i = b; i < a; ++i) {
+      ops.push_back(p.ops[i]);
+      rops.push_back(p.reg_ops[i]);
+    }
+    ph.op_mid = int(ops.size());
+    if (fuse) {
+      std::vector<cd> U(size_t(D) * D, cd());
+      for (int r = 0; r < D; ++r) U[size_t(r) * D + r] = 1.0;
+      for (int i = a; i < c; ++i) {
+        const std::vector<cd> M = reg_op_matrix(p.reg_ops[i], RB);
+        std::vector<cd> nu(size_t(D) * D, cd());
+        for (int r = 0; r < D; ++r)
+          for (int q = 0; q < D; ++q) {
+            const cd mrq = M[size_t(r) * D + q];
+            if (mrq == cd()) continue;
+            for (int s = 0; s < D; ++s) nu[size_t(r) * D + s] += mrq * U[size_t(q) * D + s];
+          }
+        U.swap(nu);
+        for (int g : p.ops[i].gates) ph.tc_gates.push_back(g);
+      }
+      ph.tc = int(p.tc_mats.size());
+      p.tc_mats.push_back(std::move(U));
+      ++ci;
+    }
+    for (int i = c; i < e; ++i) {
+      ops.push_back(p.ops[i]);
+      rops.push_back(p.reg_ops[i]);
+    }
+    ph.op_end = int(ops.size());
+  }
+  p.ops.swap(ops);
+  p.reg_ops.swap(rops);
+  p.tensor_cores = true;
 }
 
 }  // namespace
@@ -402,7 +515,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     return false;
   }
   svb_plan_options opt = opt_in;
-  int T = opt.tile_bits > 0 ? opt.tile_bits : default_tile_bits(prec);
+  // tensor-core register phases: c64 only, 12-qubit tiles (128 rows x 32 amps)
+  const bool use_tc = prec == SVB_C64 && opt.tensor_cores >= 0 && !opt.no_reg_phases &&
+                      (opt.tile_bits == 0 || opt.tile_bits == 12) && (opt.reg_bits == 0 || opt.reg_bits == 5);
+  int T = opt.tile_bits > 0 ? opt.tile_bits : (use_tc ? 12 : default_tile_bits(prec));
   // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)
   if (T > (prec == SVB_C64 ? 13 : 12)) T = prec == SVB_C64 ? 13 : 12;
   if (T > n) T = n;
@@ -413,9 +529,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   const int mmax = T - Lmin;
   const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
                           ? opt.max_ops_per_pass : kMaxOps;
-  const double budget = opt.cost_budget == 0.0 ? default_cost_budget(prec) : opt.cost_budget;
+  const double budget =
+      opt.cost_budget == 0.0 ? (use_tc ? kTcDefaultBudget : default_cost_budget(prec)) : opt.cost_budget;
   const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
-  const CostModel cm(prec);
+  const CostModel cm(prec, use_tc);
 
   plan.n = n;
   plan.prec = prec;
@@ -434,11 +551,18 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   std::vector<int> pending(gates.size());
   for (size_t i = 0; i < gates.size(); ++i) pending[i] = int(i);
 
-  while (!pending.empty()) {
-    std::vector<char> block_all(n, 0), block_dense(n, 0), in_high(n, 0);
-    int n_high = 0;
-    double cost = 0.0;
+  // One greedy scan over the pending gates.  `allowed` (optional) restricts the
+  // strided tile qubits to a window; the result is the pass it would build.
+  struct Scan {
     std::vector<int> taken, deferred;
+    std::vector<char> in_high;
+    double cost = 0.0;
+  };
+  auto scan = [&](const std::vector<int>& pend, const std::vector<char>* allowed) {
+    Scan r;
+    std::vector<char> block_all(n, 0), block_dense(n, 0);
+    r.in_high.assign(n, 0);
+    int n_high = 0;
     // Mirror of the diagonal-run merge done at lowering time, so that a
     // diagonal gate joining an open run is charged only its marginal cost and
     // the coefficient pool is accounted for with the merged table sizes.
@@ -446,7 +570,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     bool acc_open = false;
     size_t closed_pool = 0;
     const bool merging = !opt.no_diag_merge;
-    for (int gi : pending) {
+    for (int gi : pend) {
       const Gate& g = gates[gi];
       bool blocked = false;
       for (int j = 0; j < g.k && !blocked; ++j)
@@ -454,7 +578,12 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       bool take = false;
       if (!blocked) {
         int extra = 0;
-        for (int j = 0; j < g.k; ++j) extra += (g.t[j] >= Lmin && !in_high[g.t[j]]);
+        bool outside = false;
+        for (int j = 0; j < g.k; ++j)
+          if (g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+            ++extra;
+            outside |= allowed && !(*allowed)[g.t[j]];
+          }
         double c;
         size_t new_closed = closed_pool;
         std::vector<int> new_acc = acc_bits;
@@ -488,26 +617,47 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
           }
         }
         const size_t new_pool = new_closed + (new_open ? (size_t(1) << new_acc.size()) : 0);
-        take = n_high + extra <= mmax && int(taken.size()) < max_ops && new_pool <= pool_cap &&
-               (taken.empty() || budget < 0 || cost + c <= budget);
+        take = !outside && n_high + extra <= mmax && int(r.taken.size()) < max_ops && new_pool <= pool_cap &&
+               (r.taken.empty() || budget < 0 || r.cost + c <= budget);
         if (take) {
           for (int j = 0; j < g.k; ++j)
-            if (g.t[j] >= Lmin && !in_high[g.t[j]]) {
-              in_high[g.t[j]] = 1;
+            if (g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+              r.in_high[g.t[j]] = 1;
               ++n_high;
             }
-          cost += c;
+          r.cost += c;
           closed_pool = new_closed;
           acc_bits = new_acc;
           acc_open = new_open;
-          taken.push_back(gi);
+          r.taken.push_back(gi);
         }
       }
       if (!take) {
-        deferred.push_back(gi);
+        r.deferred.push_back(gi);
         for (int j = 0; j < g.k; ++j) (g.diag ? block_dense : block_all)[g.t[j]] = 1;
       }
     }
+    return r;
+  };
+
+  while (!pending.empty()) {
+    // candidate passes: the unrestricted greedy scan, and one scan per window
+    // of consecutive strided qubits; keep the one absorbing the most gates
+    Scan best = scan(pending, nullptr);
+    if (mmax > 0 && !opt.no_window_search) {
+      std::vector<char> allowed(n, 0);
+      for (int a = Lmin; a + mmax <= n; ++a) {
+        std::fill(allowed.begin(), allowed.end(), 0);
+        for (int q = a; q < a + mmax; ++q) allowed[q] = 1;
+        Scan cand = scan(pending, &allowed);
+        if (cand.taken.size() > best.taken.size() ||
+            (cand.taken.size() == best.taken.size() && cand.cost < best.cost))
+          best = std::move(cand);
+      }
+    }
+    std::vector<int>& taken = best.taken;
+    std::vector<int>& deferred = best.deferred;
+    std::vector<char>& in_high = best.in_high;
 
     // ---- tile qubit set: low Lmin qubits + chosen high ones, filled upward
     Pass p;
@@ -582,12 +732,16 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     }
     p.ops = std::move(ops);
     p.num_gates = int(taken.size());
-    int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
-    if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile
-    if (!opt.no_reg_phases && !build_phases(p, RB, prec)) {
-      p.phases.clear();
-      p.reg_ops.clear();
-      p.reg_bits = 0;
+    if (use_tc && p.T == 12 && build_phases(p, 5, prec, 7)) {
+      fuse_tc_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxTcPerPass);
+    } else {
+      int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
+      if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile
+      if (!opt.no_reg_phases && !build_phases(p, RB, prec)) {
+        p.phases.clear();
+        p.reg_ops.clear();
+        p.reg_bits = 0;
+      }
     }
     p.cost = 0.0;
     for (auto& o : p.ops) p.cost += o.kind == OP_DIAG ? cm.diag(o.k) : cm.dense(o.k);

@@ -39,6 +39,12 @@ struct RegPhase {
   int R[8] = {0};           // register bit i <-> tile-local bit R[i] (ascending)
   int op_begin = 0, op_end = 0;
   int flags = 0;
+  // tensor-core phases (k_tc_pass): ops [op_begin, op_mid) run on CUDA cores,
+  // then the fused 2^RB x 2^RB matrix tc_mats[tc] as one tcgen05 GEMM, then
+  // ops [op_mid, op_end).  tc < 0: no GEMM (op_mid == op_end).
+  int op_mid = 0;
+  int tc = -1;
+  std::vector<int> tc_gates;  // input gates folded into the GEMM, program order
 };
 struct RegOp {
   int kind = OP_DENSE;
@@ -64,6 +70,9 @@ struct Pass {
   int tma_start[5] = {0}, tma_bits[5] = {0}, tma_box[5] = {0};
   int n_enum = 0;
   int reg_bits = 0;               // > 0: executed by k_reg_pass<RB = reg_bits>
+  int thread_bits = 8;            // tile bits carried by the thread index (7 for k_tc_pass)
+  bool tensor_cores = false;      // executed by k_tc_pass
+  std::vector<std::vector<cd>> tc_mats;  // fused phase matrices (2^RB x 2^RB, row-major)
   std::vector<RegPhase> phases;
   std::vector<RegOp> reg_ops;     // same order as ops
 };

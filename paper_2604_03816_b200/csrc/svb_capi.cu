@@ -20,6 +20,7 @@
 #include "svb200.h"
 #include "svb_kernels.cuh"
 #include "svb_regpass.cuh"
+#include "svb_tcpass.cuh"
 
 using namespace svb;
 
@@ -67,7 +68,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
-                         (const void*)k_reg_pass<float2, 5>,
+                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -120,6 +121,8 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.stages = stages;
   a.h.n_phases = int(p.phases.size());
   a.h.reg_bits = p.reg_bits;
+  a.h.tc_count = p.tensor_cores ? int(p.tc_mats.size()) : 0;
+  a.h.tc_mats = nullptr;
   int off = 0;
   if (!p.phases.empty()) {
     for (size_t f = 0; f < p.phases.size(); ++f) {
@@ -127,6 +130,8 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       std::memset(&d, 0, sizeof(d));
       d.op_begin = p.phases[f].op_begin;
       d.op_end = p.phases[f].op_end;
+      d.op_mid = p.phases[f].op_mid;
+      d.tc = p.phases[f].tc;
       d.flags = p.phases[f].flags;
       for (int i = 0; i < 8; ++i) d.R[i] = p.phases[f].R[i];
     }
@@ -176,6 +181,15 @@ struct svb_plan {
   int stages = 3;
   std::vector<PassArgs<float2>> args64;
   std::vector<PassArgs<double2>> args128;
+  // tensor-core GEMM matrices of every pass, packed for the kernels (host copy
+  // built at plan time; uploaded once per device on first execution)
+  std::vector<float> tc_host;
+  std::vector<size_t> tc_offset;  // per pass, in floats
+  float* tc_dev = nullptr;
+  int tc_dev_id = -1;
+  ~svb_plan() {
+    if (tc_dev) cudaFree(tc_dev);
+  }
 };
 
 namespace {
@@ -224,6 +238,22 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   while (a.h.stages > 2 && tile_pass_smem_bytes<C>(a.h) > size_t(f->max_smem)) --a.h.stages;
   const size_t smem = tile_pass_smem_bytes<C>(a.h);
   static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
+  if constexpr (sizeof(C) == 8) {
+    if (a.h.tc_count > 0) {
+      // two CTAs per SM (TMEM 2 x 256 columns): keep each under ~113 KB
+      while (a.h.stages > 2 && tc_pass_smem_bytes(a.h) > size_t(113) * 1024) --a.h.stages;
+      const size_t smem_tc = tc_pass_smem_bytes(a.h);
+      int per_sm = 0;
+      SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_pass, kTcThreads, smem_tc));
+      if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tensor-core pass does not fit on an SM");
+      long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count * std::min(per_sm, 2));
+      if (grid < 1) grid = 1;
+      k_tc_pass<<<(unsigned)grid, kTcThreads, smem_tc, stream>>>(reinterpret_cast<float2*>(amps),
+                                                                  reinterpret_cast<const PassArgs<float2>&>(a));
+      SVB_CUDA(cudaGetLastError());
+      return SVB_OK;
+    }
+  }
   void (*fn)(C*, PassArgs<C>);
   if (a.h.n_phases > 0) {
     if constexpr (sizeof(C) == 8) {
@@ -251,8 +281,61 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   return SVB_OK;
 }
 
+// TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
+float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & ~0x1FFFu;
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
+}
+
+// K-major SWIZZLE_NONE core-matrix offset (floats) of element (n, k) of a 32x32 block
+inline int tc_bofs(int n, int k) { return ((n / 8) * 8 * 128 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) / 4; }
+
+void pack_tc(svb_plan* p) {
+  p->tc_host.clear();
+  p->tc_offset.assign(p->plan.passes.size(), 0);
+  for (size_t i = 0; i < p->plan.passes.size(); ++i) {
+    const Pass& ps = p->plan.passes[i];
+    p->tc_offset[i] = p->tc_host.size();
+    if (!ps.tensor_cores) continue;
+    for (const auto& U : ps.tc_mats) {
+      std::vector<float> blk(kTcMatBytes / 4, 0.f);
+      for (int n = 0; n < 32; ++n)
+        for (int k = 0; k < 32; ++k) {
+          const cd u = U[size_t(n) * 32 + k];
+          const float re = float(u.real()), im = float(u.imag());
+          const float rh = tf32_rna(re), ih = tf32_rna(im);
+          blk[0 * 1024 + tc_bofs(n, k)] = rh;
+          blk[1 * 1024 + tc_bofs(n, k)] = ih;
+          blk[2 * 1024 + tc_bofs(n, k)] = tf32_rna(re - rh);
+          blk[3 * 1024 + tc_bofs(n, k)] = tf32_rna(im - ih);
+        }
+      p->tc_host.insert(p->tc_host.end(), blk.begin(), blk.end());
+    }
+  }
+}
+
+int upload_tc(svb_plan* p) {
+  if (p->tc_host.empty()) return SVB_OK;
+  int dev = 0;
+  SVB_CUDA(cudaGetDevice(&dev));
+  if (p->tc_dev && p->tc_dev_id == dev) return SVB_OK;
+  if (p->tc_dev) cudaFree(p->tc_dev);
+  p->tc_dev = nullptr;
+  SVB_CUDA(cudaMalloc(&p->tc_dev, p->tc_host.size() * sizeof(float)));
+  SVB_CUDA(cudaMemcpy(p->tc_dev, p->tc_host.data(), p->tc_host.size() * sizeof(float), cudaMemcpyHostToDevice));
+  p->tc_dev_id = dev;
+  for (size_t i = 0; i < p->args64.size(); ++i)
+    p->args64[i].h.tc_mats = p->args64[i].h.tc_count ? p->tc_dev + p->tc_offset[i] : nullptr;
+  return SVB_OK;
+}
+
 template <class C>
 int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int first, int count, cudaStream_t s) {
+  if (int rc = upload_tc(p)) return rc;
   for (int i = first; i < first + count; ++i) {
     int rc = launch_pass<C>(args[i], p->plan.n, static_cast<C*>(amps), s);
     if (rc) return rc;
@@ -346,6 +429,7 @@ int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int
   std::unique_ptr<svb_plan> p(new svb_plan());
   if (!build_plan(n_local, prec, gates, o, p->plan, err)) return fail(SVB_EUNSUPPORTED, err);
   p->stages = o.stages > 0 ? std::min(o.stages, 6) : 3;
+  pack_tc(p.get());
   const int np = int(p->plan.passes.size());
   const long long n_tiles = 1LL << (n_local - (np ? p->plan.passes[0].T : 0));
   if (prec == SVB_C64) {
@@ -384,7 +468,32 @@ int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out) {
   out->est_cost = p.cost;
   out->reg_bits = p.reg_bits;
   out->num_phases = int(p.phases.size());
+  out->num_tc = p.tensor_cores ? int(p.tc_mats.size()) : 0;
   return SVB_OK;
+}
+
+int svb_plan_phase_tc(const svb_plan* plan, int pass, int phase, int* op_mid, int* tc) {
+  if (!plan || !op_mid || !tc) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (phase < 0 || phase >= int(p.phases.size())) return fail(SVB_EINVAL, "phase index out of range");
+  *op_mid = p.phases[phase].op_mid;
+  *tc = p.phases[phase].tc;
+  return SVB_OK;
+}
+
+int svb_plan_tc_matrix(const svb_plan* plan, int pass, int tc, double* out, int cap) {
+  if (!plan || !out) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (tc < 0 || tc >= int(p.tc_mats.size())) return fail(SVB_EINVAL, "tc index out of range");
+  const auto& U = p.tc_mats[tc];
+  if (int(U.size()) > cap) return fail(SVB_EINVAL, "capacity too small");
+  for (size_t e = 0; e < U.size(); ++e) {
+    out[2 * e] = U[e].real();
+    out[2 * e + 1] = U[e].imag();
+  }
+  return int(U.size());
 }
 
 int svb_plan_phase(const svb_plan* plan, int pass, int phase, int* R, int* op_begin, int* op_end, int* flags) {
@@ -426,11 +535,28 @@ int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap) {
   if (!plan || !out) return fail(SVB_EINVAL, "null argument");
   if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
   int w = 0;
-  for (const KernelOp& op : plan->plan.passes[pass].ops)
-    for (int g : op.gates) {
-      if (w >= cap) return fail(SVB_EINVAL, "output capacity too small");
-      out[w++] = g;
-    }
+  const Pass& ps = plan->plan.passes[pass];
+  auto emit = [&](int g) {
+    if (w >= cap) return false;
+    out[w++] = g;
+    return true;
+  };
+  if (ps.phases.empty()) {
+    for (const KernelOp& op : ps.ops)
+      for (int g : op.gates)
+        if (!emit(g)) return fail(SVB_EINVAL, "output capacity too small");
+    return w;
+  }
+  for (const RegPhase& ph : ps.phases) {
+    for (int i = ph.op_begin; i < ph.op_mid; ++i)
+      for (int g : ps.ops[i].gates)
+        if (!emit(g)) return fail(SVB_EINVAL, "output capacity too small");
+    for (int g : ph.tc_gates)
+      if (!emit(g)) return fail(SVB_EINVAL, "output capacity too small");
+    for (int i = ph.op_mid; i < ph.op_end; ++i)
+      for (int g : ps.ops[i].gates)
+        if (!emit(g)) return fail(SVB_EINVAL, "output capacity too small");
+  }
   return w;
 }
 

@@ -258,7 +258,7 @@ __host__ __device__ inline size_t tile_pass_smem_bytes(const PassHeader& h) {
 // ------------------------------------------------------------------ kernel
 template <class C, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1) k_tile_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const int S = h.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed   (1 arrival + tx)

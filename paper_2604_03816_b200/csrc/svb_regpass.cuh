@@ -172,7 +172,7 @@ template <class C, int RB>
 __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + 8;
   constexpr int NR = 1 << RB;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const int S = h.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed (1 arrival + tx bytes)

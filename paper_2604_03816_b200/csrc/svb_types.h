@@ -43,9 +43,16 @@ constexpr int kMaxPhases = 32;
 enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2 };
 
 struct PhaseDesc {
-  int op_begin, op_end, flags, pad;
+  int op_begin, op_end, flags, tc;  // tc >= 0: tensor-core GEMM tc between [op_begin,op_mid) and [op_mid,op_end)
+  int op_mid, pad0, pad1, pad2;
   int R[8];
 };
+
+// k_tc_pass: fused phase matrices as TF32 hi/lo pairs in the K-major
+// SWIZZLE_NONE core-matrix layout (8 rows x 16 B core matrices, LBO 128 B,
+// SBO 1024 B): [Ur_hi | Ui_hi | Ur_lo | Ui_lo], 32 x 32 fp32 each.
+constexpr int kTcMatBytes = 4 * 32 * 32 * 4;
+constexpr int kMaxTcPerPassDev = 2;
 
 struct PassHeader {
   int T, L, m, n_ops;
@@ -66,6 +73,9 @@ struct PassHeader {
   // the non-tile bits in runs: origin = sum ((tile >> src) & (2^len-1)) << dst
   int n_gap_runs;
   int gap_src[kMaxHigh + 1], gap_dst[kMaxHigh + 1], gap_len[kMaxHigh + 1];
+  int tc_count;                 // fused GEMM matrices of this pass (k_tc_pass)
+  int tc_pad;
+  const float* tc_mats;         // device: tc_count * kTcMatBytes (set at launch)
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)

@@ -165,24 +165,32 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
     for p in range(nat.num_passes()):
         info = nat.pass_info(p)
         T, rb = info["tile_bits"], info["reg_bits"]
-        assert rb > 0 and T == rb + 8
+        assert rb > 0 and T - rb in (7, 8)
         nr = 1 << rb
+        nthreads = 1 << (T - rb)
         phases = [nat.phase(p, f) for f in range(info["num_phases"])]
         ops = [nat.phase_op(p, i) for i in range(info["num_kernel_ops"])]
-        tid = np.arange(256)
+        tid = np.arange(nthreads)
         for tile in range(1 << (n - T)):
             idx = tile_indices(n, info, tile)
             buf = amps[idx].copy()
             for ph in phases:
                 R = ph["R"][:rb]
                 nonr = [q for q in range(T) if q not in R]
-                base = np.zeros(256, dtype=np.int64)
+                base = np.zeros(nthreads, dtype=np.int64)
                 for k, q in enumerate(nonr):
                     base |= ((tid >> k) & 1) << q
                 loc = np.stack([base + sum(1 << R[i] for i in range(rb) if (rho >> i) & 1)
                                 for rho in range(nr)], axis=1)
                 v = buf[loc]
-                for o in range(ph["op_begin"], ph["op_end"]):
+                order = list(range(ph["op_begin"], ph["op_mid"])) + ["tc"] + \
+                    list(range(ph["op_mid"], ph["op_end"]))
+                for o in order:
+                    if o == "tc":
+                        if ph["tc"] >= 0:
+                            U = nat.tc_matrix(p, ph["tc"]).astype(v.dtype)
+                            v[:] = v @ U.T
+                        continue
                     op = ops[o]
                     if op["kind"] == "dense":
                         k, mask = op["k"], op["mask"]
@@ -198,7 +206,7 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                     else:
                         kt = op["mask"]
                         kr = op["k"] - kt
-                        dt = np.zeros(256, dtype=np.int64)
+                        dt = np.zeros(nthreads, dtype=np.int64)
                         for j, tb in enumerate(op["thread_bits"]):
                             dt |= ((tid >> tb) & 1) << (kr + j)
                         tab = op["coeffs"].astype(v.dtype)
@@ -241,3 +249,25 @@ def test_register_phase_encoding_other_widths(prec, rb):
         assert all(i["reg_bits"] == rb for i in infos)
         got = emulate_reg(plan, circ.num_qubits, prec)
         assert np.abs(got - want).max() <= (1e-12 if prec == "double" else 1e-5)
+
+
+@pytest.mark.parametrize("name,make", REG_CASES, ids=[c[0] for c in REG_CASES])
+def test_tensor_core_phase_encoding(name, make):
+    """k_tc_pass plans (c64): phases whose dense gates fuse into one 32x32
+    matrix; emulated with the planner's fused matrices."""
+    c = make()
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(c.num_qubits, Precision.SINGLE, c.gates, plan_options(tensor_cores=1))
+    infos = plan.passes()
+    assert all(i["tile_bits"] == 12 and i["reg_bits"] == 5 for i in infos)
+    got = emulate_reg(plan, c.num_qubits, "single")
+    assert np.abs(got - want).max() <= 1e-5
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+
+
+def test_tensor_core_plans_layered28():
+    f, _ = fuse(gen.layered_circuit(28), 2)
+    plan = CircuitPlan(28, Precision.SINGLE, f.gates, plan_options(tensor_cores=1))
+    infos = plan.passes()
+    assert sum(i["num_tc"] for i in infos) > 0
+    assert len(infos) < 26
