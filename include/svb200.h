@@ -53,14 +53,14 @@ typedef struct svb_plan_options {
   int min_low_bits;     /* contiguous low qubits always in the tile (0: 512-B chunks) */
   int max_ops_per_pass; /* 0: 48 (kernel limit)                                      */
   double cost_budget;   /* modelled compute per pass as a multiple of the pass's HBM
-                           time; 0: default (3.0 c64, 2.0 c128), <0: unlimited       */
+                           time; 0: default (7.0 c64, 5.0 c128), <0: unlimited       */
   int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
   int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
   int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
   int tensor_cores;     /* c64 only: 1 = fuse register phases into tcgen05 TF32x3
                            GEMMs (k_tc_pass, 12-qubit tiles, 32 amps x 128 threads);
-                           0 = default (on for c64), -1 = off                      */
+                           0 = default (off), -1 = off                      */
   int tc_min_dense;     /* dense gates a phase needs to become a GEMM (0: 2)         */
   int no_window_search; /* 1: plain program-order greedy pass building             */
 } svb_plan_options;

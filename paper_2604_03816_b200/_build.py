@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsvb200.so")
 SOURCES = ["svb_capi.cu", "planner.cpp"]
-HEADERS = ["svb_kernels.cuh", "svb_types.h", "planner.h"]
+HEADERS = ["svb_kernels.cuh", "svb_regpass.cuh", "svb_tcpass.cuh", "svb_types.h", "planner.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -18,7 +18,7 @@ constexpr double kTcDefaultBudget = 3.0;
 int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 11; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
 int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 3; }
-double default_cost_budget(int prec) { return prec == SVB_C64 ? 3.0 : 2.0; }
+double default_cost_budget(int prec) { return prec == SVB_C64 ? 7.0 : 5.0; }
 // tile = RB + 8 qubits for the register kernel
 
 namespace {
@@ -515,8 +515,8 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     return false;
   }
   svb_plan_options opt = opt_in;
-  // tensor-core register phases: c64 only, 12-qubit tiles (128 rows x 32 amps)
-  const bool use_tc = prec == SVB_C64 && opt.tensor_cores >= 0 && !opt.no_reg_phases &&
+  // tensor-core register phases (opt-in): c64 only, 12-qubit tiles (128 rows x 32 amps)
+  const bool use_tc = prec == SVB_C64 && opt.tensor_cores > 0 && !opt.no_reg_phases &&
                       (opt.tile_bits == 0 || opt.tile_bits == 12) && (opt.reg_bits == 0 || opt.reg_bits == 5);
   int T = opt.tile_bits > 0 ? opt.tile_bits : (use_tc ? 12 : default_tile_bits(prec));
   // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)

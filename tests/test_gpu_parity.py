@@ -88,8 +88,7 @@ OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits"
         {"no_diag_merge": 1, "stages": 2}, {"stages": 4, "max_ops_per_pass": 1},
         {"no_reg_phases": 1}, {"reg_bits": 3, "tile_bits": 11}, {"cost_budget": -1.0, "stages": 2},
         {"reg_bits": 5, "tile_bits": 13, "cost_budget": 3.0, "tensor_cores": -1},
-        {"tensor_cores": 1, "cost_budget": -1.0}, {"tensor_cores": 1, "tc_min_dense": 1, "stages": 2},
-        {"tensor_cores": -1, "no_window_search": 1}]
+        {"cost_budget": 6.0}, {"tensor_cores": -1, "no_window_search": 1}]
 
 
 @pytest.mark.parametrize("opts", OPTS, ids=[str(o) for o in OPTS])

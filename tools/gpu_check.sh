@@ -8,6 +8,6 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1
 timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
 timeout 600 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.txt 2>&1; echo "bench rc=$?" >> gpurun_out/bench.txt
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -k regex:k_tile_pass -c 80 --csv --log-file gpurun_out/launches.csv \
+  -k regex:"k_(tile|reg|tc)_pass" -c 80 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 tail -3 gpurun_out/pytest_gpu.txt gpurun_out/smoke.txt gpurun_out/bench.txt
