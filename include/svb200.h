@@ -55,7 +55,8 @@ typedef struct svb_plan_options {
   double cost_budget;   /* modelled compute per pass as a multiple of the pass's HBM
                            time; 0: default (7.0 c64, 5.0 c128), <0: unlimited       */
   int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
-  int stages;           /* TMA pipeline depth per CTA (0: 3)                         */
+  int stages;           /* TMA pipeline depth per CTA (0: deepest ring that keeps the
+                           CTAs per SM of a 2-stage ring)                         */
   int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
   int tensor_cores;     /* c64 only: 1 = fuse register phases into tcgen05 TF32x3
@@ -120,11 +121,16 @@ int svb_plan_phase_tc(const svb_plan* plan, int pass, int phase, int* op_mid, in
  * row-major, register-bit order) for tests. */
 int svb_plan_tc_matrix(const svb_plan* plan, int pass, int tc, double* out, int cap);
 /* Register-phase encoding of kernel op i.  Dense: *mask = register-bit mask.
- * Diagonal: *mask = kt, src[0..kt) = thread bits of table bits kr..; src must
- * hold 2 * SVB_MAX_TARGETS ints: src[8..15] viewed as 32 bytes map each rho
- * to the register part of the table index. */
+ * Diagonal: table index = [thread bits | register bits | outside-tile bits];
+ * *mask = kt, src[0..kt) = thread bits of table bits 0..kt; src must hold
+ * 2 * SVB_MAX_TARGETS ints: src[8..15] viewed as 32 bytes map each rho to
+ * the register part of the table index (already shifted by kt). */
 int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
                       double* coeffs, int coeff_cap);
+/* Diagonal op i: the top *kx table-index bits are shard qubits outside the
+ * tile (set bits of *xmask, ascending), constant over a tile.  svb_plan_kernel_op
+ * reports such a target as tile_bits + qubit. */
+int svb_plan_phase_op_ext(const svb_plan* plan, int pass, int i, int* kx, unsigned long long* xmask);
 int svb_plan_execute(svb_plan* plan, void* amps, void* stream);
 int svb_plan_execute_range(svb_plan* plan, void* amps, int first_pass, int num_passes, void* stream);
 void svb_plan_destroy(svb_plan* plan);

@@ -23,7 +23,7 @@ EXPORTS = (
     "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
     "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
-    "svb_plan_phase_tc", "svb_plan_tc_matrix",
+    "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext",
     "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
     "svb_probabilities", "svb_block_sums", "svb_sample_search",
@@ -80,6 +80,7 @@ def lib():
         "svb_plan_phase": (i, [vp, i, i, ip, ip, ip, ip]),
         "svb_plan_phase_op": (i, [vp, i, i, ip, ip, ip, ip, dp, i]),
         "svb_plan_phase_tc": (i, [vp, i, i, ip, ip]),
+        "svb_plan_phase_op_ext": (i, [vp, i, i, ip, C.POINTER(C.c_ulonglong)]),
         "svb_plan_tc_matrix": (i, [vp, i, i, dp, i]),
         "svb_plan_execute": (i, [vp, vp, vp]),
         "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
@@ -177,6 +178,10 @@ class NativePlan:
         if kind.value == 1:
             out["thread_bits"] = [int(x) for x in src[:mask.value]]
             out["rmap"] = src[8:16].view(np.uint8).copy()
+            kx, xm = C.c_int(), C.c_ulonglong()
+            check(lib().svb_plan_phase_op_ext(self._h, p, i, C.byref(kx), C.byref(xm)))
+            out["ext_qubits"] = [q for q in range(64) if (xm.value >> q) & 1]
+            assert len(out["ext_qubits"]) == kx.value
         return out
 
     def pass_gates(self, p: int) -> list[int]:

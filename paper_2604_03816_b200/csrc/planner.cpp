@@ -145,7 +145,8 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       const KernelOp& op = p.ops[i];
       bool blocked = false;
       for (int j = 0; j < op.k && !blocked; ++j)
-        blocked = block_all[op.tgt[j]] || (op.kind == OP_DENSE && block_dense[op.tgt[j]]);
+        blocked = op.tgt[j] < p.T &&
+                  (block_all[op.tgt[j]] || (op.kind == OP_DENSE && block_dense[op.tgt[j]]));
       bool take = false;
       if (!blocked) {
         if (op.kind == OP_DIAG) {
@@ -164,7 +165,8 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
         took.push_back(i);
       } else {
         rest.push_back(i);
-        for (int j = 0; j < op.k; ++j) (op.kind == OP_DIAG ? block_dense : block_all)[op.tgt[j]] = 1;
+        for (int j = 0; j < op.k; ++j)
+          if (op.tgt[j] < p.T) (op.kind == OP_DIAG ? block_dense : block_all)[op.tgt[j]] = 1;
       }
     }
     sets.push_back(R);
@@ -193,7 +195,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       const KernelOp& op = p.ops[i];
       if (op.kind != OP_DIAG) continue;
       for (int j = op.k - 1; j >= 0 && int(R.size()) < RB; --j)
-        if (op.tgt[j] >= low_conflict && std::find(R.begin(), R.end(), op.tgt[j]) == R.end())
+        if (op.tgt[j] >= low_conflict && op.tgt[j] < p.T && std::find(R.begin(), R.end(), op.tgt[j]) == R.end())
           R.push_back(op.tgt[j]);
     }
     for (int b = p.T - 1; b >= 0 && int(R.size()) < RB; --b)
@@ -224,9 +226,15 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       ro.kind = op.kind;
       ro.k = op.k;
       if (op.kind == OP_DIAG) {
-        // new table index = [register-sourced bits asc. by register | thread bits asc.]
-        std::vector<std::pair<int, int>> regb, thrb;  // (register idx / thread bit, op bit)
+        // new table index = [thread bits asc. | register-sourced bits asc. by register
+        //                    | shard bits outside the tile, asc.]: lanes of a warp that
+        // differ in thread bits read adjacent table entries (no bank conflicts)
+        std::vector<std::pair<int, int>> regb, thrb, extb;  // (register idx / thread bit / qubit, op bit)
         for (int b = 0; b < op.k; ++b) {
+          if (op.tgt[b] >= p.T) {
+            extb.push_back({op.tgt[b] - p.T, b});
+            continue;
+          }
           const int r = reg_of(op.tgt[b]);
           if (r >= 0)
             regb.push_back({r, b});
@@ -235,19 +243,24 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
         }
         std::sort(regb.begin(), regb.end());
         std::sort(thrb.begin(), thrb.end());
-        const int kr = int(regb.size()), kt = int(thrb.size());
+        std::sort(extb.begin(), extb.end());
+        const int kr = int(regb.size()), kt = int(thrb.size()), kx = int(extb.size());
         ro.mask = kt;  // stored in OpDesc.pad
         for (int j = 0; j < kt; ++j) ro.src[j] = thrb[j].first;
+        ro.kx = kx;
+        ro.xmask = 0;
+        for (int j = 0; j < kx; ++j) ro.xmask |= 1ULL << extb[j].first;
         for (int rho = 0; rho < (1 << RB); ++rho) {
           int d = 0;
-          for (int j = 0; j < kr; ++j) d |= ((rho >> regb[j].first) & 1) << j;
+          for (int j = 0; j < kr; ++j) d |= ((rho >> regb[j].first) & 1) << (kt + j);
           ro.rmap[rho] = static_cast<unsigned char>(d);
         }
         ro.coeff.assign(op.coeff.size(), cd());
         for (size_t nidx = 0; nidx < op.coeff.size(); ++nidx) {
           int old = 0;
-          for (int j = 0; j < kr; ++j) old |= ((int(nidx) >> j) & 1) << regb[j].second;
-          for (int j = 0; j < kt; ++j) old |= ((int(nidx) >> (kr + j)) & 1) << thrb[j].second;
+          for (int j = 0; j < kt; ++j) old |= ((int(nidx) >> j) & 1) << thrb[j].second;
+          for (int j = 0; j < kr; ++j) old |= ((int(nidx) >> (kt + j)) & 1) << regb[j].second;
+          for (int j = 0; j < kx; ++j) old |= ((int(nidx) >> (kr + kt + j)) & 1) << extb[j].second;
           ro.coeff[nidx] = op.coeff[old];
         }
       } else {
@@ -319,7 +332,8 @@ void fuse_tc_phases(Pass& p, int min_dense, int max_tc) {
     int best = -1, ba = 0, bc = 0;
     for (int a = ph.op_begin; a < ph.op_end;) {
       int c = a, dense = 0;
-      while (c < ph.op_end && (p.reg_ops[c].kind == OP_DENSE || p.reg_ops[c].mask == 0)) {
+      while (c < ph.op_end &&
+             (p.reg_ops[c].kind == OP_DENSE || (p.reg_ops[c].mask == 0 && p.reg_ops[c].kx == 0))) {
         dense += p.reg_ops[c].kind == OP_DENSE;
         ++c;
       }
@@ -540,8 +554,9 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   plan.passes.clear();
 
   for (size_t i = 0; i < gates.size(); ++i) {
-    int high_needed = 0;
-    for (int j = 0; j < gates[i].k; ++j) high_needed += gates[i].t[j] >= Lmin;
+    int high_needed = 0;  // diagonal gates need no tile qubits (bits outside the tile are per-tile constants)
+    if (!gates[i].diag)
+      for (int j = 0; j < gates[i].k; ++j) high_needed += gates[i].t[j] >= Lmin;
     if (high_needed > mmax) {
       err = "gate " + std::to_string(i) + " needs more strided tile bits than the tile allows";
       return false;
@@ -569,6 +584,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     std::vector<int> acc_bits;
     bool acc_open = false;
     size_t closed_pool = 0;
+    int n_kops = 0;  // kernel ops after merging (what max_ops bounds)
     const bool merging = !opt.no_diag_merge;
     for (int gi : pend) {
       const Gate& g = gates[gi];
@@ -580,7 +596,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
         int extra = 0;
         bool outside = false;
         for (int j = 0; j < g.k; ++j)
-          if (g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+          if (!g.diag && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
             ++extra;
             outside |= allowed && !(*allowed)[g.t[j]];
           }
@@ -588,6 +604,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
         size_t new_closed = closed_pool;
         std::vector<int> new_acc = acc_bits;
         bool new_open = acc_open;
+        int new_kops = n_kops + 1;
         if (!merging) {
           c = cm.of(g);
           new_closed += g.m.size();
@@ -598,6 +615,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
           if (acc_open && int(u.size()) <= kMaxDiagK) {
             c = cm.diag(int(u.size())) - cm.diag(int(acc_bits.size()));
             new_acc = u;
+            new_kops = n_kops;
           } else {
             if (acc_open) new_closed += size_t(1) << acc_bits.size();
             c = cm.diag(g.k);
@@ -617,15 +635,16 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
           }
         }
         const size_t new_pool = new_closed + (new_open ? (size_t(1) << new_acc.size()) : 0);
-        take = !outside && n_high + extra <= mmax && int(r.taken.size()) < max_ops && new_pool <= pool_cap &&
+        take = !outside && n_high + extra <= mmax && new_kops <= max_ops && new_pool <= pool_cap &&
                (r.taken.empty() || budget < 0 || r.cost + c <= budget);
         if (take) {
           for (int j = 0; j < g.k; ++j)
-            if (g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+            if (!g.diag && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
               r.in_high[g.t[j]] = 1;
               ++n_high;
             }
           r.cost += c;
+          n_kops = new_kops;
           closed_pool = new_closed;
           acc_bits = new_acc;
           acc_open = new_open;
@@ -695,8 +714,20 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     };
 
     // ---- lower to kernel ops, merging diagonal runs
+    // diagonal gates: qubits outside the tile are encoded as T + qubit
+    auto dloc = [&](int q) {
+      const int l = local(q);
+      return l >= 0 ? l : p.T + q;
+    };
     auto lower_plain = [&](int gi) {
       const Gate& g = gates[gi];
+      if (g.diag) {  // sorted table bits (shard bits outside the tile last)
+        int tg[kMaxK];
+        for (int j = 0; j < g.k; ++j) tg[j] = dloc(g.t[j]);
+        DiagAcc one;
+        one.absorb(tg, g.k, g.m, gi);
+        return one.take();
+      }
       KernelOp op;
       op.kind = g.diag ? OP_DIAG : OP_DENSE;
       op.k = g.k;
@@ -712,7 +743,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       for (int gi : taken) {
         const Gate& g = gates[gi];
         int tg[kMaxK];
-        for (int j = 0; j < g.k; ++j) tg[j] = local(g.t[j]);
+        for (int j = 0; j < g.k; ++j) tg[j] = g.diag ? dloc(g.t[j]) : local(g.t[j]);
         if (g.diag) {
           if (!acc.empty() && acc.union_size(tg, g.k) > kMaxDiagK) ops.push_back(acc.take());
           acc.absorb(tg, g.k, g.m, gi);
@@ -729,6 +760,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     if (!merge) {
       ops.clear();
       for (int gi : taken) ops.push_back(lower_plain(gi));
+    }
+    if (int(ops.size()) > kMaxOps) {
+      err = "internal planner error: kernel ops per pass";
+      return false;
     }
     p.ops = std::move(ops);
     p.num_gates = int(taken.size());

@@ -29,7 +29,9 @@ struct Gate {
 struct KernelOp {
   int kind = OP_DENSE;
   int k = 0;
-  int tgt[kMaxK] = {0};    // tile-local bits, matrix-local bit j -> tgt[j]
+  int tgt[kMaxK] = {0};    // tile-local bits, matrix-local bit j -> tgt[j]; diagonal ops
+                           // only: tgt >= T is shard qubit tgt - T outside the tile
+                           // (always the top table bits, ascending)
   std::vector<cd> coeff;
   std::vector<int> gates;  // input gates folded into this op, program order
 };
@@ -52,6 +54,8 @@ struct RegOp {
   int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
   int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
   unsigned char rmap[32] = {0};  // diagonal: register part of the table index per rho
+  int kx = 0;                     // diagonal: top kx table bits are shard qubits outside the tile
+  unsigned long long xmask = 0;   //   (ascending), selected per tile from the tile origin
   std::vector<cd> coeff;   // dense: matrix permuted to ascending register bits
 };
 

@@ -146,6 +146,9 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       if (ro.kind == OP_DIAG) {
         std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
+        d.kx = ro.kx;
+        d.xmask = ro.xmask;
+        if (ro.kx) a.h.has_outside = 1;
       }
       for (const cd& z : ro.coeff) {
         a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
@@ -163,8 +166,15 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
     d.kind = ko.kind;
     d.k = ko.k;
     d.coeff_off = off;
-    for (int j = 0; j < ko.k; ++j) d.tgt[j] = d.srt[j] = ko.tgt[j];
-    std::sort(d.srt, d.srt + ko.k);
+    for (int j = 0; j < ko.k; ++j) {
+      if (ko.kind == OP_DIAG && ko.tgt[j] >= p.T) {  // shard bit outside the tile
+        ++d.kx;
+        d.xmask |= 1ULL << (ko.tgt[j] - p.T);
+        continue;
+      }
+      d.tgt[j] = d.srt[j] = ko.tgt[j];
+    }
+    std::sort(d.srt, d.srt + ko.k - d.kx);
     for (const cd& z : ko.coeff) {
       a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
       a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
@@ -234,13 +244,14 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     // tensor map refused (should not happen for planned shapes): 1-D bulk copies
     a.h.tma_rank = 0;
   }
-  // deepest TMA ring that fits the opt-in shared memory (>= 2 stages)
-  while (a.h.stages > 2 && tile_pass_smem_bytes<C>(a.h) > size_t(f->max_smem)) --a.h.stages;
-  const size_t smem = tile_pass_smem_bytes<C>(a.h);
+  auto smem_of = [&]() {
+    return a.h.n_phases > 0 ? reg_smem_layout<C>(a.h).total : tile_pass_smem_bytes<C>(a.h);
+  };
   static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
   if constexpr (sizeof(C) == 8) {
     if (a.h.tc_count > 0) {
       // two CTAs per SM (TMEM 2 x 256 columns): keep each under ~113 KB
+      if (a.h.stages == 0) a.h.stages = 3;
       while (a.h.stages > 2 && tc_pass_smem_bytes(a.h) > size_t(113) * 1024) --a.h.stages;
       const size_t smem_tc = tc_pass_smem_bytes(a.h);
       int per_sm = 0;
@@ -269,6 +280,27 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
       if (a.ops[i].kind == OP_DENSE) kmax = std::max(kmax, a.ops[i].k);
     fn = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
   }
+  if (a.h.stages == 0) {
+    // Automatic TMA ring depth: the deepest ring that keeps the CTAs per SM of
+    // a 2-stage ring (measured: resident warps matter more than ring depth --
+    // qft-30 c128 141 ms at 2 stages / 2 CTAs vs 192 ms at 3 stages / 1 CTA).
+    a.h.stages = 2;
+    int occ2 = 0, occ = 0;
+    SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, kThreads, smem_of()));
+    while (a.h.stages < 6) {
+      ++a.h.stages;
+      occ = 0;
+      if (smem_of() <= size_t(f->max_smem))
+        SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem_of()));
+      if (occ < occ2) {
+        --a.h.stages;
+        break;
+      }
+    }
+  }
+  // deepest TMA ring that fits the opt-in shared memory (>= 2 stages)
+  while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
+  const size_t smem = smem_of();
   int per_sm = 0;
   SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
   if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tile pass does not fit on an SM (shared memory)");
@@ -428,7 +460,7 @@ int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int
   if (!make_gates(n_local, n_ops, op_k, op_targets, op_mats, gates, err)) return fail(SVB_EINVAL, err);
   std::unique_ptr<svb_plan> p(new svb_plan());
   if (!build_plan(n_local, prec, gates, o, p->plan, err)) return fail(SVB_EUNSUPPORTED, err);
-  p->stages = o.stages > 0 ? std::min(o.stages, 6) : 3;
+  p->stages = o.stages > 0 ? std::max(2, std::min(o.stages, 6)) : 0;  // 0: chosen at first launch
   pack_tc(p.get());
   const int np = int(p->plan.passes.size());
   const long long n_tiles = 1LL << (n_local - (np ? p->plan.passes[0].T : 0));
@@ -529,6 +561,16 @@ int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, 
     }
   }
   return int(op.coeff.size());
+}
+
+int svb_plan_phase_op_ext(const svb_plan* plan, int pass, int i, int* kx, unsigned long long* xmask) {
+  if (!plan || !kx || !xmask) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (i < 0 || i >= int(p.reg_ops.size())) return fail(SVB_EINVAL, "op index out of range");
+  *kx = p.reg_ops[i].kx;
+  *xmask = p.reg_ops[i].xmask;
+  return SVB_OK;
 }
 
 int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap) {

@@ -198,18 +198,31 @@ __device__ __forceinline__ void tile_dense(C* __restrict__ buf, const OpDesc& op
   }
 }
 
-// Diagonal op (a merged run of diagonal gates): amp[e] *= table[bits of e at tgt].
+// Bits of `x` selected by `mask`, packed ascending (software PEXT).
+__device__ __forceinline__ int pext_bits(long long x, unsigned long long mask) {
+  int r = 0, b = 0;
+  while (mask) {
+    const int q = __ffsll((long long)mask) - 1;
+    r |= int((x >> q) & 1) << b++;
+    mask &= mask - 1;
+  }
+  return r;
+}
+
+// Diagonal op (a merged run of diagonal gates): amp[e] *= table[bits of e at
+// tgt | shard bits of the tile origin at xmask].
 template <class C>
 __device__ __forceinline__ void tile_diag(C* __restrict__ buf, const OpDesc& op, const C* __restrict__ pool,
-                                          int T, int tid) {
+                                          int T, int tid, long long origin) {
   const C* table = pool + op.coeff_off;
-  const int k = op.k;
+  const int k = op.k - op.kx;
   int tg[kMaxK];
 #pragma unroll
   for (int b = 0; b < kMaxK; ++b) tg[b] = b < k ? op.tgt[b] : 0;
+  const int dx = op.kx ? pext_bits(origin, op.xmask) << k : 0;
   const int N = 1 << T;
   for (int e = tid; e < N; e += kComputeThreads) {
-    int d = 0;
+    int d = dx;
 #pragma unroll
     for (int b = 0; b < kMaxK; ++b)
       if (b < k) d |= ((e >> tg[b]) & 1) << b;
@@ -220,9 +233,10 @@ __device__ __forceinline__ void tile_diag(C* __restrict__ buf, const OpDesc& op,
 // KMAX bounds the dense arity compiled into a kernel variant, so the common
 // (fused width <= 2) variant carries no register pressure from wide gates.
 template <class C, int KMAX>
-__device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* pool, int T, int tid) {
+__device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* pool, int T, int tid,
+                                           long long origin) {
   if (op.kind == OP_DIAG) {
-    tile_diag<C>(buf, op, pool, T, tid);
+    tile_diag<C>(buf, op, pool, T, tid, origin);
     return;
   }
   switch (op.k) {
@@ -323,9 +337,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_pass(C* __restrict__ amps,
       const int s = int(it % S);
       mbar_wait(&full[s], uint32_t((it / S) & 1));
       C* buf = tiles + size_t(s) * tile_elems;
+      const long long origin = tile_base((long long)blockIdx.x + it * gridDim.x, h);
       for (int o = 0; o < h.n_ops; ++o) {
         if (o) compute_bar();
-        tile_apply<C, KMAX>(buf, args.ops[o], pool, h.T, tid);
+        tile_apply<C, KMAX>(buf, args.ops[o], pool, h.T, tid, origin);
       }
       fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk store
       mbar_arrive(&done[s]);

@@ -46,9 +46,15 @@ __device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__
   constexpr int K = popc_c(MASK);
   constexpr int D = 1 << K;
   constexpr int REST = ((1 << RB) - 1) & ~MASK;
-  C M[D * D];
+  // matrices up to 2q (c64 and c128) are hoisted into registers (measured:
+  // per-use shared-memory broadcasts cost 12% on layered c128); wider ones
+  // are read per use
+  constexpr bool kHoist = D <= 4;
+  C M[kHoist ? D * D : 1];
+  if constexpr (kHoist) {
 #pragma unroll
-  for (int e = 0; e < D * D; ++e) M[e] = Ms[e];
+    for (int e = 0; e < D * D; ++e) M[e] = Ms[e];
+  }
 #pragma unroll
   for (int g = 0; g < (1 << (RB - K)); ++g) {
     const int base = deposit_mask<RB>(g, REST);
@@ -59,39 +65,48 @@ __device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__
     for (int i = 0; i < D; ++i) {
       C acc = czero<C>();
 #pragma unroll
-      for (int j = 0; j < D; ++j) acc = cfma(M[i * D + j], in[j], acc);
+      for (int j = 0; j < D; ++j) {
+        if constexpr (kHoist) acc = cfma(M[i * D + j], in[j], acc);
+        else acc = cfma(Ms[i * D + j], in[j], acc);
+      }
       v[base | deposit_mask<RB>(i, MASK)] = acc;
     }
   }
 }
 
-// Diagonal op.  The planner orders the table index as [register-sourced bits
-// | thread-sourced bits]: rmap packs, per register index rho, the register
-// part of the table index (4 bits per rho); the thread part is gathered once
-// per tile from the thread bits listed in op.srt[0..kt).
-template <class C, int RB>
-__device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, const C* __restrict__ table, int tid) {
-  const int kt = op.pad;
-  const int kr = op.k - kt;
+// Diagonal op.  The planner orders the table index as [thread-sourced bits |
+// register-sourced bits | shard bits outside the tile]: rmap packs, per
+// register index rho, the register part of the table index (one byte per
+// rho, already shifted); the thread part depends only on the thread and the
+// outside part only on the tile, so both are precomputed (dbase) -- see
+// diag_base and k_reg_pass.  Thread bits lowest: lanes that differ in them
+// read adjacent entries, so the lookups are bank-conflict free.
+__device__ __forceinline__ int diag_thread_part(const OpDesc& op, int tid) {
   int dt = 0;
 #pragma unroll
   for (int j = 0; j < kMaxK; ++j)
-    if (j < kt) dt |= ((tid >> op.srt[j]) & 1) << j;
-  dt <<= kr;
+    if (j < op.pad) dt |= ((tid >> op.srt[j]) & 1) << j;
+  return dt;
+}
+__device__ __forceinline__ int diag_outside_part(const OpDesc& op, long long origin) {
+  return op.kx ? pext_bits(origin, op.xmask) << (op.k - op.kx) : 0;
+}
+__device__ __forceinline__ int diag_base(const OpDesc& op, int tid, long long origin) {
+  return diag_thread_part(op, tid) | diag_outside_part(op, origin);
+}
+
+template <class C, int RB>
+__device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, const C* __restrict__ table, int dbase) {
 #pragma unroll
   for (int rho = 0; rho < (1 << RB); ++rho) {
-    const int d = dt | ((op.tgt[rho >> 2] >> (8 * (rho & 3))) & 0xff);
+    const int d = dbase | ((op.tgt[rho >> 2] >> (8 * (rho & 3))) & 0xff);
     v[rho] = cmul(v[rho], table[d]);
   }
 }
 
 template <class C, int RB>
-__device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, const C* pool, int tid) {
+__device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool) {
   const C* co = pool + op.coeff_off;
-  if (op.kind == OP_DIAG) {
-    reg_diag<C, RB>(v, op, co, tid);
-    return;
-  }
   switch (op.pad) {  // register-bit mask of the dense op
 #define SVB_CASE(m) \
   case m:           \
@@ -104,6 +119,30 @@ __device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, con
 #undef SVB_CASE
     default: break;
   }
+}
+
+template <class C, int RB>
+__device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, const C* pool, int dbase) {
+  if (op.kind == OP_DIAG)
+    reg_diag<C, RB>(v, op, pool + op.coeff_off, dbase);
+  else
+    reg_dense_op<C, RB>(v, op, pool);
+}
+
+// Shared-memory layout of k_reg_pass: barriers | coefficient pool | thread
+// parts of the diagonal table indices | outside-tile parts (2S ring) | tiles.
+struct RegSmem {
+  size_t pool, dthr, dout, tiles, total;
+};
+template <class C>
+__host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
+  RegSmem l;
+  l.pool = 128;
+  l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(C), 128);
+  l.dout = l.dthr + align_up(size_t(h.n_ops) * kComputeThreads, 128);
+  l.tiles = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
+  l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
+  return l;
 }
 
 // Per-thread addressing of one phase.  The tile-local index of register rho
@@ -177,8 +216,11 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
   const int S = h.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed (1 arrival + tx bytes)
   uint64_t* empty = full + S;                           // tile buffer drained (256 arrivals)
-  C* pool = reinterpret_cast<C*>(smem + 128);
-  C* tiles = reinterpret_cast<C*>(smem + 128 + align_up(size_t(h.coeff_count) * sizeof(C), 128));
+  const RegSmem lay = reg_smem_layout<C>(h);
+  C* pool = reinterpret_cast<C*>(smem + lay.pool);
+  unsigned char* dthr = smem + lay.dthr;  // [op][tid]: thread part of each diagonal table index
+  int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
+  C* tiles = reinterpret_cast<C*>(smem + lay.tiles);
   const int tid = threadIdx.x;
 
   if (tid == 0) {
@@ -189,7 +231,18 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
     fence_mbar_init();
   }
   for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  for (int e = tid; e < h.n_ops * kComputeThreads; e += kThreads) {
+    const OpDesc& op = args.ops[e / kComputeThreads];
+    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % kComputeThreads) : 0;
+  }
   __syncthreads();
+  // outside-tile table bits of tile `it` (written by the producer before it
+  // arms the stage's barrier; a 2S ring so a slot outlives its buffer)
+  auto publish_outside = [&](int xs, long long tile) {
+    const long long o = tile_base(tile, h);
+    int* slot = dout + xs * kMaxOps;
+    for (int i = 0; i < h.n_ops; ++i) slot[i] = args.ops[i].kind == OP_DIAG ? diag_outside_part(args.ops[i], o) : 0;
+  };
 
   const long long n_tiles = h.n_tiles;
   const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -203,10 +256,11 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
       if (lane != 0) return;
       const int ne = h.n_enum;
       const int sub = T - ne;
-      int s = 0;
+      int s = 0, xs = 0;
       uint32_t ph = 0;  // parity of the use of buffer s
-      for (long long it = 0; it < mine; ++it) {
+      for (long long it = 0; it < mine; ++it, xs = xs + 1 == 2 * S ? 0 : xs + 1) {
         if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
+        if (h.has_outside) publish_outside(xs, (long long)blockIdx.x + it * gridDim.x);
         mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
         const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
         C* buf = tiles + (size_t(s) << T);
@@ -235,7 +289,10 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
       const int s = int(it % S);
       if (it >= S) mbar_wait_sleep(&empty[s], uint32_t(((it - S) / S) & 1));
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
+      if (lane == 0) {
+        if (h.has_outside) publish_outside(int(it % (2 * S)), (long long)blockIdx.x + it * gridDim.x);
+        mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
+      }
       __syncwarp();
       const long long base = tile_base((long long)blockIdx.x + it * gridDim.x, h);
       C* buf = tiles + (size_t(s) << T);
@@ -261,11 +318,13 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
 #pragma unroll
     for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.R[i], h);
   }
-  int s = 0;
+  int s = 0, xs = 0;
   uint32_t parity = 0;
-  for (long long it = 0; it < mine; ++it, (++s == S ? (s = 0, parity ^= 1) : 0)) {
+  for (long long it = 0; it < mine;
+       ++it, (++s == S ? (s = 0, parity ^= 1) : 0), xs = xs + 1 == 2 * S ? 0 : xs + 1) {
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
+    const long long origin = tile_base(tile, h);
     mbar_wait(&full[s], parity);
     C v[NR];
     for (int p = 0; p < np; ++p) {
@@ -296,13 +355,20 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
       if (last && !tout) mbar_arrive(&empty[s]);  // buffer free for the next load
-      for (int o = ph.op_begin; o < ph.op_end; ++o) reg_apply<C, RB>(v, args.ops[o], pool, tid);
+      for (int o = ph.op_begin; o < ph.op_end; ++o) {
+        const OpDesc& op = args.ops[o];
+        if (op.kind == OP_DIAG)
+          reg_diag<C, RB>(v, op, pool + op.coeff_off,
+                          int(dthr[o * kComputeThreads + tid]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
+        else
+          reg_dense_op<C, RB>(v, op, pool);
+      }
       if (!last) {
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
       } else if (!tout) {
         // direct store from registers (coalesced: R avoids the bank-row bits)
-        C* __restrict__ dst = amps + tile_base(tile, h) + last_g.gthr;
+        C* __restrict__ dst = amps + origin + last_g.gthr;
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[last_g.at(r) - last_g.gthr] = v[r];
       } else {
@@ -310,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
         compute_bar();
-        C* __restrict__ dst = amps + tile_base(tile, h);
+        C* __restrict__ dst = amps + origin;
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * kComputeThreads + tid)];
         mbar_arrive(&empty[s]);

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
   for (long long it = 0; it < mine; ++it, (++s == S ? (s = 0, parity ^= 1) : 0)) {
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
+    const long long origin = tile_base(tile, h);
     mbar_wait(&full[s], parity);
     C v[NR];
     for (int p = 0; p < np; ++p) {
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
       if (last && !tout) mbar_arrive(&empty[s]);
-      for (int o = ph.op_begin; o < ph.op_mid; ++o) reg_apply<C, RB>(v, args.ops[o], pool, tid);
+      for (int o = ph.op_begin; o < ph.op_mid; ++o) reg_apply<C, RB>(v, args.ops[o], pool, args.ops[o].kind == OP_DIAG ? diag_base(args.ops[o], tid, origin) : 0);
       if (ph.tc >= 0) {
         // ---- fused phase matrix on the tensor cores
         {
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
         }
         tc_fence_before();
       }
-      for (int o = ph.op_mid; o < ph.op_end; ++o) reg_apply<C, RB>(v, args.ops[o], pool, tid);
+      for (int o = ph.op_mid; o < ph.op_end; ++o) reg_apply<C, RB>(v, args.ops[o], pool, args.ops[o].kind == OP_DIAG ? diag_base(args.ops[o], tid, origin) : 0);
       if (!last) {
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];

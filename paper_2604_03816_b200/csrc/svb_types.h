@@ -32,6 +32,13 @@ struct OpDesc {
   int pad;
   int tgt[kMaxK];     // tile-local bit acted on by matrix-local bit j
   int srt[kMaxK];     // tgt sorted ascending (zero-bit insertion order)
+  // Diagonal ops only: the top kx table-index bits are shard qubits OUTSIDE
+  // the tile (ascending, mask xmask).  They are constant over a tile, so a
+  // diagonal gate never needs its qubits in the tile: its factor for those
+  // bits is selected per tile from the tile origin.
+  int kx;
+  int pad2;
+  unsigned long long xmask;
 };
 
 // Register-resident execution (k_reg_pass): a pass is a list of phases; in
@@ -74,7 +81,7 @@ struct PassHeader {
   int n_gap_runs;
   int gap_src[kMaxHigh + 1], gap_dst[kMaxHigh + 1], gap_len[kMaxHigh + 1];
   int tc_count;                 // fused GEMM matrices of this pass (k_tc_pass)
-  int tc_pad;
+  int has_outside;              // some diagonal op reads shard bits outside the tile
   const float* tc_mats;         // device: tc_count * kTcMatBytes (set at launch)
 };
 

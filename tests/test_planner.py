@@ -51,7 +51,8 @@ def emulate(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                     d = np.zeros(1 << T, dtype=np.int64)
                     e = np.arange(1 << T)
                     for b, t in enumerate(op["targets"]):
-                        d |= ((e >> t) & 1) << b
+                        # t >= T: shard qubit t - T outside the tile (per-tile constant)
+                        d |= (((e >> t) if t < T else (idx >> (t - T))) & 1) << b
                     buf *= op["coeffs"].astype(buf.dtype)[d]
             amps[idx] = buf
     return amps
@@ -205,10 +206,13 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                                 v[:, cols[i]] = vin @ M[i]
                     else:
                         kt = op["mask"]
-                        kr = op["k"] - kt
+                        kx = len(op["ext_qubits"])
+                        kr = op["k"] - kt - kx
                         dt = np.zeros(nthreads, dtype=np.int64)
                         for j, tb in enumerate(op["thread_bits"]):
-                            dt |= ((tid >> tb) & 1) << (kr + j)
+                            dt |= ((tid >> tb) & 1) << j
+                        for j, q in enumerate(op["ext_qubits"]):
+                            dt |= (int(idx[0] >> q) & 1) << (kr + kt + j)
                         tab = op["coeffs"].astype(v.dtype)
                         for rho in range(nr):
                             v[:, rho] *= tab[dt | int(op["rmap"][rho])]
@@ -271,3 +275,23 @@ def test_tensor_core_plans_layered28():
     infos = plan.passes()
     assert sum(i["num_tc"] for i in infos) > 0
     assert len(infos) < 26
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_diagonal_gates_outside_the_tile(prec):
+    """Diagonal gates need no tile qubits: bits outside the tile are constant
+    per tile and select the table entry from the tile origin.  QFT stages then
+    share passes (qft-30 c128: 53 passes before, <= 12 now)."""
+    c = fuse(gen.qft_circuit(16), 2)[0]
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(16, Precision(prec), c.gates)
+    infos = plan.passes()
+    ext = 0
+    for p, info in enumerate(infos):
+        for i in range(info["num_kernel_ops"]):
+            ext += any(t >= info["tile_bits"] for t in plan.native.kernel_op(p, i)["targets"])
+    assert ext > 0
+    got = emulate_reg(plan, 16, prec)
+    assert np.abs(got - want).max() <= (1e-12 if prec == "double" else 1e-5)
+    f30, _ = fuse(gen.qft_circuit(30), 2)
+    assert CircuitPlan(30, Precision.DOUBLE, f30.gates).num_passes <= 12
