@@ -140,6 +140,29 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def plan_kernels(plan) -> str:
+    """Kernel(s) the plan launches (register-phase / shared-memory / tensor-core)."""
+    names = set()
+    for p in range(plan.num_passes):
+        info = plan.native.pass_info(p)
+        names.add("k_tc_pass" if info["num_tc"] else
+                  f"k_reg_pass<RB={info['reg_bits']}>" if info["reg_bits"] else "k_tile_pass")
+    return "+".join(sorted(names))
+
+
+def measured_traffic(cfg: str, prec: str, n: int):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernel from the committed ncu --set full capture of this workload
+    (profiles/traffic.json), or None when no capture exists."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            ent = json.load(fh).get(f"{cfg}:{prec}:{n}")
+        return None if ent is None else ent["bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def measured_peak_hbm():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -318,6 +341,24 @@ def run_b200(args):
             e2e_times.append(dt)
     e2e_value = g0 / statistics.median(e2e_times)
 
+    # compute roofline of the same launches: algorithmic flops of the fused
+    # gates (dense k-qubit: 8*2^k - 2 real flops per amplitude, diagonal: 6)
+    # against the vector FMA peak of the precision (FP32 128 / FP64 64 FMA per
+    # clock per SM at the sampled max SM clock)
+    from paper_2604_03816_b200.circuit import effective_unitary as _eu
+    flops_amp = 0
+    for op in fused.gates:
+        u = _eu(op)
+        k = len(op.targets)
+        flops_amp += 6 if np.count_nonzero(u - np.diag(np.diag(u))) == 0 else 8 * (1 << k) - 2
+    clk_summary = clk.summary()
+    sm_mhz = clk_summary.get("sm_max_mhz") or 1965.0
+    fma_per_clk = 128 if prec == "single" else 64
+    dev_props = torch.cuda.get_device_properties(local)
+    peak_tflops = dev_props.multi_processor_count * fma_per_clk * 2 * sm_mhz * 1e6 / 1e12
+    achieved_tflops = flops_amp * (1 << n) / (sum(pass_ms) / 1e3) / 1e12
+    traffic = measured_traffic(cfg, prec, n)
+
     cpu = None
     if not args.no_cpu_baseline:
         torch.cuda.empty_cache()
@@ -337,15 +378,21 @@ def run_b200(args):
                    "circuit_ms": ms_step, "fused_gates_per_s": gf / (ms_step / 1e3),
                    "passes_per_s": n_passes / (ms_step / 1e3), "norm_after": norm},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "k_tile_pass", "bytes_per_launch": bytes_per_pass,
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": plan_kernels(plan), "bytes_per_launch": bytes_per_pass,
                      "avg_launch_ms": avg_pass_ms, "best_launch_ms": best_pass,
-                     "best_frac": bytes_per_pass / (best_pass / 1e3) / 1e9 / peak},
+                     "best_frac": bytes_per_pass / (best_pass / 1e3) / 1e9 / peak,
+                     "compute": {"bound": "fp32-fma" if prec == "single" else "fp64-fma",
+                                 "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                                 "frac": achieved_tflops / peak_tflops,
+                                 "flops_per_amp": flops_amp,
+                                 "note": "vector FMA peak = SMs x FMA/clk x 2 x max SM clock; "
+                                         "the passes are HBM- or FMA-bound, whichever is larger"}},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8 + (8 if pc == 0 else 16),
                 "path": "B200Engine.run_circuit(fused circuit) + norm_squared + amplitude[0] read"},
         "gpu_launches": args.steps * (n_passes + 2),
-        "clocks": clk.summary(),
+        "clocks": clk_summary,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))

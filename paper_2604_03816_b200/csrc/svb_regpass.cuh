@@ -237,11 +237,14 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
   }
   __syncthreads();
   // outside-tile table bits of tile `it` (written by the producer before it
-  // arms the stage's barrier; a 2S ring so a slot outlives its buffer)
-  auto publish_outside = [&](int xs, long long tile) {
+  // arms the stage's barrier; a 2S ring so a slot outlives its buffer).  The
+  // whole producer warp computes it, one op per lane.
+  auto publish_outside = [&](int xs, long long tile, int lane) {
     const long long o = tile_base(tile, h);
     int* slot = dout + xs * kMaxOps;
-    for (int i = 0; i < h.n_ops; ++i) slot[i] = args.ops[i].kind == OP_DIAG ? diag_outside_part(args.ops[i], o) : 0;
+    for (int i = lane; i < h.n_ops; i += 32)
+      slot[i] = args.ops[i].kind == OP_DIAG ? diag_outside_part(args.ops[i], o) : 0;
+    __syncwarp();
   };
 
   const long long n_tiles = h.n_tiles;
@@ -253,18 +256,18 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
     if (h.tma_rank > 0) {
       // one tensor-map load per (enumerated) sub-box: a single UTMALDG per tile
       // whenever the tile's qubit runs fit a rank-5 tensor map
-      if (lane != 0) return;
+      if (lane != 0 && !h.has_outside) return;
       const int ne = h.n_enum;
       const int sub = T - ne;
       int s = 0, xs = 0;
       uint32_t ph = 0;  // parity of the use of buffer s
       for (long long it = 0; it < mine; ++it, xs = xs + 1 == 2 * S ? 0 : xs + 1) {
         if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
-        if (h.has_outside) publish_outside(xs, (long long)blockIdx.x + it * gridDim.x);
-        mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
+        if (h.has_outside) publish_outside(xs, (long long)blockIdx.x + it * gridDim.x, lane);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
         const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
         C* buf = tiles + (size_t(s) << T);
-        for (int e = 0; e < (1 << ne); ++e) {
+        for (int e = 0; e < (lane == 0 ? 1 << ne : 0); ++e) {
           long long origin = tb;
           for (int j = 0; j < ne; ++j)
             if ((e >> j) & 1) origin += 1LL << h.high[h.m - ne + j];
@@ -289,10 +292,8 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
       const int s = int(it % S);
       if (it >= S) mbar_wait_sleep(&empty[s], uint32_t(((it - S) / S) & 1));
       __syncwarp();
-      if (lane == 0) {
-        if (h.has_outside) publish_outside(int(it % (2 * S)), (long long)blockIdx.x + it * gridDim.x);
-        mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
-      }
+      if (h.has_outside) publish_outside(int(it % (2 * S)), (long long)blockIdx.x + it * gridDim.x, lane);
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
       __syncwarp();
       const long long base = tile_base((long long)blockIdx.x + it * gridDim.x, h);
       C* buf = tiles + (size_t(s) << T);
