@@ -59,9 +59,10 @@ typedef struct svb_plan_options {
                            CTAs per SM of a 2-stage ring)                         */
   int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
-  int tensor_cores;     /* c64 only: 1 = fuse register phases into tcgen05 TF32x3
-                           GEMMs (k_tc_pass, 12-qubit tiles, 32 amps x 128 threads);
-                           0 = default (off), -1 = off                      */
+  int tensor_cores;     /* c64 only: 2 = fuse whole register phases into warp-level
+                           tensor-core GEMMs (mma.sync f16 hi/lo, in k_reg_pass);
+                           1 = tcgen05 TF32x3 GEMMs (k_tc_pass, 12-qubit tiles,
+                           experimental); 0 = default (2 for c64), -1 = off */
   int tc_min_dense;     /* dense gates a phase needs to become a GEMM (0: 2)         */
   int no_window_search; /* 1: plain program-order greedy pass building             */
 } svb_plan_options;
@@ -127,6 +128,10 @@ int svb_plan_tc_matrix(const svb_plan* plan, int pass, int tc, double* out, int 
  * the register part of the table index (already shifted by kt). */
 int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, int* mask, int* src,
                       double* coeffs, int coeff_cap);
+/* Thread-local layout of register phase `phase`: map16[i] = tile bit of
+ * register-index bit i (i < reg_bits), map16[reg_bits + b] = tile bit of
+ * thread-index bit b; *mma = 1 for a tensor-core (mma.sync) GEMM phase. */
+int svb_plan_phase_map(const svb_plan* plan, int pass, int phase, int* map16, int* mma);
 /* Diagonal op i: the top *kx table-index bits are shard qubits outside the
  * tile (set bits of *xmask, ascending), constant over a tile.  svb_plan_kernel_op
  * reports such a target as tile_bits + qubit. */

@@ -23,7 +23,7 @@ EXPORTS = (
     "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
     "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
-    "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext",
+    "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext", "svb_plan_phase_map",
     "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
     "svb_probabilities", "svb_block_sums", "svb_sample_search",
@@ -81,6 +81,7 @@ def lib():
         "svb_plan_phase_op": (i, [vp, i, i, ip, ip, ip, ip, dp, i]),
         "svb_plan_phase_tc": (i, [vp, i, i, ip, ip]),
         "svb_plan_phase_op_ext": (i, [vp, i, i, ip, C.POINTER(C.c_ulonglong)]),
+        "svb_plan_phase_map": (i, [vp, i, i, ip, ip]),
         "svb_plan_tc_matrix": (i, [vp, i, i, dp, i]),
         "svb_plan_execute": (i, [vp, vp, vp]),
         "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
@@ -158,8 +159,11 @@ class NativePlan:
         check(lib().svb_plan_phase(self._h, p, f, R, C.byref(b), C.byref(e), C.byref(fl)))
         mid, tc = C.c_int(), C.c_int()
         check(lib().svb_plan_phase_tc(self._h, p, f, C.byref(mid), C.byref(tc)))
+        mp = (C.c_int * 16)()
+        mma = C.c_int()
+        check(lib().svb_plan_phase_map(self._h, p, f, mp, C.byref(mma)))
         return {"R": list(R), "op_begin": b.value, "op_end": e.value, "flags": fl.value,
-                "op_mid": mid.value, "tc": tc.value}
+                "op_mid": mid.value, "tc": tc.value, "map": list(mp), "mma": bool(mma.value)}
 
     def tc_matrix(self, p: int, tc: int) -> np.ndarray:
         out = np.zeros(2 * 1024, dtype=np.float64)

@@ -119,6 +119,21 @@ struct DiagAcc {
 
 size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 
+// Transposes around the first / last phase: the TMA buffer (linear tile
+// layout) is read, and the last phase stores to HBM, directly in the phase's
+// layout only when the lane bits cover the bank-row index bits (conflict-free
+// shared-memory reads, coalesced stores); otherwise through a swizzled
+// shared-memory transpose.
+void set_layout_flags(RegPhase& rp, int RB, int prec, bool first, bool last) {
+  const int low_conflict = prec == SVB_C64 ? 4 : 3;  // bank-row index bits
+  int lanes = 0;  // tile bits of the lanes of one shared-memory wavefront
+  for (int b = 0; b < low_conflict; ++b) lanes |= 1 << rp.map[RB + b];
+  const bool low = lanes != (1 << low_conflict) - 1;
+  rp.flags &= ~(PH_TRANSPOSE_IN | PH_TRANSPOSE_OUT);
+  if (first && low) rp.flags |= PH_TRANSPOSE_IN;
+  if (last && low) rp.flags |= PH_TRANSPOSE_OUT;
+}
+
 // Partition a lowered pass into register phases (k_reg_pass).  Phases are
 // list-scheduled: each phase scans the remaining ops in order and takes every
 // op whose predecessors (earlier ops on a shared bit, diagonal pairs excepted)
@@ -206,9 +221,12 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
     for (int i = 0; i < RB; ++i) rp.R[i] = R[i];
     rp.op_begin = ranges[ph].first;
     rp.op_end = ranges[ph].second;
-    const bool low = R[0] < low_conflict;
-    if (ph == 0 && low) rp.flags |= PH_TRANSPOSE_IN;
-    if (ph + 1 == sets.size() && low) rp.flags |= PH_TRANSPOSE_OUT;
+    // register-FMA layout: register-index bit i <-> R[i], thread bits <-> the
+    // other tile bits ascending
+    for (int i = 0; i < RB; ++i) rp.map[i] = R[i];
+    for (int q = 0, j = 0; q < p.T; ++q)
+      if (std::find(R.begin(), R.end(), q) == R.end()) rp.map[RB + j++] = q;
+    set_layout_flags(rp, RB, prec, ph == 0, ph + 1 == sets.size());
     auto reg_of = [&](int t) {
       for (int i = 0; i < RB; ++i)
         if (R[i] == t) return i;
@@ -396,6 +414,130 @@ void fuse_tc_phases(Pass& p, int min_dense, int max_tc) {
   p.tensor_cores = true;
 }
 
+// Turn up to max_mma whole register phases (c64, RB 5, 8 thread bits) whose
+// ops all act on register bits only into one fused 32x32 matrix each,
+// executed by k_reg_pass as a warp-level tensor-core GEMM (mma.sync m16n8k16,
+// fp16 hi/lo split with per-row power-of-two scaling).  The GEMM phase uses the
+// fragment layout: with the phase's register set R ascending (the matrix-local
+// bit order) and the other 8 tile bits r0..r7 ascending,
+//   register-index bits 0..4 <-> R[2], R[3], R[4], r3, r4
+//   thread-index bits  0..7 <-> R[0], R[1], r0, r1, r2, r5, r6, r7
+// so lane = 4 g + c holds complex columns i = c + 4 m (m = register bits 0..2)
+// of the rows g, g + 8, g + 16, g + 24 (register bits 3, 4) of its warp.
+void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
+  const int RB = p.reg_bits;
+  if (RB != 5 || p.thread_bits != 8 || prec != SVB_C64) return;
+  const int D = 1 << RB;
+  struct Cand { int dense, phase; };
+  std::vector<Cand> cands;
+  for (int f = 0; f < int(p.phases.size()); ++f) {
+    const RegPhase& ph = p.phases[f];
+    int dense = 0;
+    bool ok = ph.op_end > ph.op_begin;
+    for (int i = ph.op_begin; i < ph.op_end && ok; ++i) {
+      const RegOp& ro = p.reg_ops[i];
+      if (ro.kind == OP_DENSE) ++dense;
+      else ok = ro.mask == 0 && ro.kx == 0;  // diagonal on register bits only
+    }
+    if (ok && dense >= min_dense) cands.push_back({dense, f});
+  }
+  if (cands.empty()) return;
+  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {
+    return x.dense != y.dense ? x.dense > y.dense : x.phase < y.phase;
+  });
+  if (int(cands.size()) > max_mma) cands.resize(max_mma);
+  std::vector<char> chosen(p.phases.size(), 0);
+  for (const Cand& c : cands) chosen[c.phase] = 1;
+  std::vector<KernelOp> ops;
+  std::vector<RegOp> rops;
+  p.tc_mats.clear();
+  for (int f = 0; f < int(p.phases.size()); ++f) {
+    RegPhase& ph = p.phases[f];
+    const int b = ph.op_begin, e = ph.op_end;
+    ph.op_begin = int(ops.size());
+    if (chosen[f]) {
+      std::vector<cd> U(size_t(D) * D, cd());
+      for (int r = 0; r < D; ++r) U[size_t(r) * D + r] = 1.0;
+      for (int i = b; i < e; ++i) {
+        const std::vector<cd> M = reg_op_matrix(p.reg_ops[i], RB);
+        std::vector<cd> nu(size_t(D) * D, cd());
+        for (int r = 0; r < D; ++r)
+          for (int q = 0; q < D; ++q) {
+            const cd mrq = M[size_t(r) * D + q];
+            if (mrq == cd()) continue;
+            for (int t = 0; t < D; ++t) nu[size_t(r) * D + t] += mrq * U[size_t(q) * D + t];
+          }
+        U.swap(nu);
+        for (int g : p.ops[i].gates) ph.tc_gates.push_back(g);
+      }
+      ph.tc = int(p.tc_mats.size());
+      p.tc_mats.push_back(std::move(U));
+      ph.mma = true;
+      ph.flags |= PH_MMA;
+      // row bits: g0, g1 (lanes 2, 3) complete the bank positions of the
+      // half-warp together with R[0], R[1] (lanes 0, 1): tile bit t lands on
+      // bank-row position t mod 4 under the XOR swizzle, and on t itself in
+      // the linear TMA layout -- prefer exactly {0..3}, else distinct
+      // residues; g2 (lane 4) then prefers bit 4 (256-B coalesced stores)
+      std::vector<int> rows;
+      for (int q = 0; q < p.T; ++q)
+        if (std::find(ph.R, ph.R + RB, q) == ph.R + RB) rows.push_back(q);
+      std::vector<int> pick;
+      auto take_row = [&](int q) {
+        rows.erase(std::find(rows.begin(), rows.end(), q));
+        pick.push_back(q);
+      };
+      int used = (1 << (ph.R[0] & 3)) | (1 << (ph.R[1] & 3));
+      for (int want = 0; want < 2; ++want) {
+        int best = -1;
+        for (int q : rows) {
+          const bool fresh = !((used >> (q & 3)) & 1);
+          const int score = (fresh ? 2 : 0) + (q < 4 ? 1 : 0);
+          const int bscore = best < 0 ? -1 : (!((used >> (best & 3)) & 1) ? 2 : 0) + (best < 4 ? 1 : 0);
+          if (score > bscore) best = q;
+        }
+        used |= 1 << (best & 3);
+        take_row(best);
+      }
+      take_row(std::find(rows.begin(), rows.end(), 4) != rows.end() ? 4 : rows[0]);
+      const int lay[13] = {ph.R[2], ph.R[3], ph.R[4], rows[0], rows[1],
+                           ph.R[0], ph.R[1], pick[0], pick[1], pick[2], rows[2], rows[3], rows[4]};
+      for (int i = 0; i < 13; ++i) ph.map[i] = lay[i];
+      set_layout_flags(ph, RB, prec, f == 0, f + 1 == int(p.phases.size()));
+    } else {
+      for (int i = b; i < e; ++i) {
+        ops.push_back(p.ops[i]);
+        rops.push_back(p.reg_ops[i]);
+      }
+    }
+    ph.op_mid = ph.op_end = int(ops.size());
+  }
+  p.ops.swap(ops);
+  p.reg_ops.swap(rops);
+  p.mma_phases = true;
+  // all ops of the pass unitary (|U^dagger U - 1| <= 1e-9, diagonal |z| = 1):
+  // the tile 2-norm is invariant and the kernel restores it
+  auto unitary = [](const std::vector<cd>& m, int d) {
+    for (int r = 0; r < d; ++r)
+      for (int t = 0; t < d; ++t) {
+        cd acc = 0.0;
+        for (int q = 0; q < d; ++q) acc += std::conj(m[size_t(q) * d + r]) * m[size_t(q) * d + t];
+        if (std::abs(acc - (r == t ? cd(1.0) : cd(0.0))) > 1e-9) return false;
+      }
+    return true;
+  };
+  bool ok = true;
+  for (const auto& U : p.tc_mats) ok = ok && unitary(U, D);
+  for (const KernelOp& op : p.ops) {
+    if (op.kind == OP_DIAG) {
+      for (const cd& z : op.coeff) ok = ok && std::abs(std::abs(z) - 1.0) <= 1e-9;
+    } else {
+      ok = ok && unitary(op.coeff, 1 << op.k);
+    }
+  }
+  p.renorm = ok;
+}
+
 }  // namespace
 
 // Decide the TMA tensor-map shape of a pass and the tile-local order of its
@@ -530,7 +672,12 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   }
   svb_plan_options opt = opt_in;
   // tensor-core register phases (opt-in): c64 only, 12-qubit tiles (128 rows x 32 amps)
-  const bool use_tc = prec == SVB_C64 && opt.tensor_cores > 0 && !opt.no_reg_phases &&
+  // tensor_cores == 2: warp-level mma.sync GEMM phases inside k_reg_pass (c64)
+  // (default for c64: measured layered-28 46 ms vs 55 ms on the FMA pipes)
+  const bool use_mma = prec == SVB_C64 && (opt.tensor_cores == 2 || opt.tensor_cores == 0) &&
+                       !opt.no_reg_phases &&
+                       (opt.reg_bits == 0 || opt.reg_bits == 5);
+  const bool use_tc = prec == SVB_C64 && opt.tensor_cores == 1 && !opt.no_reg_phases &&
                       (opt.tile_bits == 0 || opt.tile_bits == 12) && (opt.reg_bits == 0 || opt.reg_bits == 5);
   int T = opt.tile_bits > 0 ? opt.tile_bits : (use_tc ? 12 : default_tile_bits(prec));
   // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)
@@ -776,6 +923,8 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
         p.phases.clear();
         p.reg_ops.clear();
         p.reg_bits = 0;
+      } else if (use_mma && p.reg_bits == 5 && p.T == 13) {
+        fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);
       }
     }
     p.cost = 0.0;

@@ -47,6 +47,9 @@ struct RegPhase {
   int op_mid = 0;
   int tc = -1;
   std::vector<int> tc_gates;  // input gates folded into the GEMM, program order
+  // thread-local layout (see PhaseDesc::map); filled by build_phases
+  int map[16] = {0};
+  bool mma = false;           // k_reg_pass mma.sync GEMM phase (whole phase = tc_mats[tc])
 };
 struct RegOp {
   int kind = OP_DENSE;
@@ -76,6 +79,8 @@ struct Pass {
   int reg_bits = 0;               // > 0: executed by k_reg_pass<RB = reg_bits>
   int thread_bits = 8;            // tile bits carried by the thread index (7 for k_tc_pass)
   bool tensor_cores = false;      // executed by k_tc_pass
+  bool mma_phases = false;        // k_reg_pass with mma.sync GEMM phases (tc_mats)
+  bool renorm = false;            // all ops unitary: the kernel restores each tile's norm
   std::vector<std::vector<cd>> tc_mats;  // fused phase matrices (2^RB x 2^RB, row-major)
   std::vector<RegPhase> phases;
   std::vector<RegOp> reg_ops;     // same order as ops

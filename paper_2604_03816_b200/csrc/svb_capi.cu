@@ -5,6 +5,7 @@
 // grid = SMs x resident CTAs), error mapping.  No device memory is owned by a
 // plan; reductions use stream-ordered scratch (cudaMallocAsync).
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
@@ -121,7 +122,9 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.stages = stages;
   a.h.n_phases = int(p.phases.size());
   a.h.reg_bits = p.reg_bits;
-  a.h.tc_count = p.tensor_cores ? int(p.tc_mats.size()) : 0;
+  a.h.tc_count = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
+  a.h.mma_phases = p.mma_phases ? 1 : 0;
+  a.h.renorm = p.renorm ? 1 : 0;
   a.h.tc_mats = nullptr;
   int off = 0;
   if (!p.phases.empty()) {
@@ -134,6 +137,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       d.tc = p.phases[f].tc;
       d.flags = p.phases[f].flags;
       for (int i = 0; i < 8; ++i) d.R[i] = p.phases[f].R[i];
+      for (int i = 0; i < 16; ++i) d.map[i] = static_cast<unsigned char>(p.phases[f].map[i]);
     }
     for (size_t i = 0; i < p.reg_ops.size(); ++i) {
       const RegOp& ro = p.reg_ops[i];
@@ -249,7 +253,7 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   };
   static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
   if constexpr (sizeof(C) == 8) {
-    if (a.h.tc_count > 0) {
+    if (a.h.tc_count > 0 && !a.h.mma_phases) {
       // two CTAs per SM (TMEM 2 x 256 columns): keep each under ~113 KB
       if (a.h.stages == 0) a.h.stages = 3;
       while (a.h.stages > 2 && tc_pass_smem_bytes(a.h) > size_t(113) * 1024) --a.h.stages;
@@ -326,12 +330,56 @@ float tf32_rna(float x) {
 // K-major SWIZZLE_NONE core-matrix offset (floats) of element (n, k) of a 32x32 block
 inline int tc_bofs(int n, int k) { return ((n / 8) * 8 * 128 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) / 4; }
 
+// mma.sync m16n8k16 B fragments of the real block form of a 32x32 complex
+// phase matrix U (v_out = U v_in): B[2i + a][2j + b] with
+// B[2i][2j] = Re U[j][i], B[2i+1][2j] = -Im U[j][i], B[2i][2j+1] = Im U[j][i],
+// B[2i+1][2j+1] = Re U[j][i]; split B = Bh + Bl (fp16, round to nearest).
+// Fragment (nt, kk), lane = 4 g + c: b0 = B[16kk + 2c + {0,1}][8nt + g],
+// b1 = B[16kk + 8 + 2c + {0,1}][8nt + g] (lower k in the low half).
+void pack_mma(const std::vector<cd>& U, std::vector<float>& out) {
+  auto Bv = [&](int k, int n) -> double {
+    const int i = k >> 1, a = k & 1, j = n >> 1, b = n & 1;
+    const cd u = U[size_t(j) * 32 + i];
+    if (a == 0) return b == 0 ? u.real() : u.imag();
+    return b == 0 ? -u.imag() : u.real();
+  };
+  auto split = [](double x, uint16_t& h, uint16_t& l) {
+    const float f = float(x);
+    const __half hh = __float2half_rn(f);
+    const __half ll = __float2half_rn(f - __half2float(hh));
+    std::memcpy(&h, &hh, 2);
+    std::memcpy(&l, &ll, 2);
+  };
+  const size_t base = out.size();
+  out.resize(base + kMmaMatBytes / 4);
+  uint32_t* w = reinterpret_cast<uint32_t*>(out.data() + base);
+  for (int nt = 0; nt < 8; ++nt)
+    for (int kk = 0; kk < 4; ++kk)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, c = lane & 3, n = 8 * nt + g;
+        uint16_t h[4], l[4];
+        split(Bv(16 * kk + 2 * c, n), h[0], l[0]);
+        split(Bv(16 * kk + 2 * c + 1, n), h[1], l[1]);
+        split(Bv(16 * kk + 8 + 2 * c, n), h[2], l[2]);
+        split(Bv(16 * kk + 8 + 2 * c + 1, n), h[3], l[3]);
+        uint32_t* q = w + ((nt * 4 + kk) * 32 + lane) * 4;
+        q[0] = uint32_t(h[0]) | (uint32_t(h[1]) << 16);
+        q[1] = uint32_t(h[2]) | (uint32_t(h[3]) << 16);
+        q[2] = uint32_t(l[0]) | (uint32_t(l[1]) << 16);
+        q[3] = uint32_t(l[2]) | (uint32_t(l[3]) << 16);
+      }
+}
+
 void pack_tc(svb_plan* p) {
   p->tc_host.clear();
   p->tc_offset.assign(p->plan.passes.size(), 0);
   for (size_t i = 0; i < p->plan.passes.size(); ++i) {
     const Pass& ps = p->plan.passes[i];
     p->tc_offset[i] = p->tc_host.size();
+    if (ps.mma_phases) {
+      for (const auto& U : ps.tc_mats) pack_mma(U, p->tc_host);
+      continue;
+    }
     if (!ps.tensor_cores) continue;
     for (const auto& U : ps.tc_mats) {
       std::vector<float> blk(kTcMatBytes / 4, 0.f);
@@ -500,7 +548,7 @@ int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out) {
   out->est_cost = p.cost;
   out->reg_bits = p.reg_bits;
   out->num_phases = int(p.phases.size());
-  out->num_tc = p.tensor_cores ? int(p.tc_mats.size()) : 0;
+  out->num_tc = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
   return SVB_OK;
 }
 
@@ -561,6 +609,16 @@ int svb_plan_phase_op(const svb_plan* plan, int pass, int i, int* kind, int* k, 
     }
   }
   return int(op.coeff.size());
+}
+
+int svb_plan_phase_map(const svb_plan* plan, int pass, int phase, int* map16, int* mma) {
+  if (!plan || !map16 || !mma) return fail(SVB_EINVAL, "null argument");
+  if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
+  const Pass& p = plan->plan.passes[pass];
+  if (phase < 0 || phase >= int(p.phases.size())) return fail(SVB_EINVAL, "phase index out of range");
+  for (int i = 0; i < 16; ++i) map16[i] = p.phases[phase].map[i];
+  *mma = p.phases[phase].mma ? 1 : 0;
+  return SVB_OK;
 }
 
 int svb_plan_phase_op_ext(const svb_plan* plan, int pass, int i, int* kx, unsigned long long* xmask) {

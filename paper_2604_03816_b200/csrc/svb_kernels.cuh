@@ -43,17 +43,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting thread is suspended in
+// hardware until the phase completes (or the hint expires), so waiting warps
+// take no issue slots from the compute warps sharing their scheduler.
+__device__ __forceinline__ bool mbar_try_wait_suspend(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) {
+  while (!mbar_try_wait_suspend(a, parity)) {
   }
 }
-// Producer-side wait: back off with nanosleep so a waiting producer warp does
-// not steal issue slots from the compute warps sharing its scheduler.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_addr(bar);
-  while (!mbar_try_wait(a, parity)) __nanosleep(800);
-}
+// Producer-side wait (same primitive; kept as a separate name for call sites
+// that previously backed off with nanosleep).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar,
                                           uint64_t policy) {
   asm volatile(

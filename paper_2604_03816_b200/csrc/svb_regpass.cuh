@@ -58,19 +58,23 @@ __device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__
 #pragma unroll
   for (int g = 0; g < (1 << (RB - K)); ++g) {
     const int base = deposit_mask<RB>(g, REST);
-    C in[D];
+    // input-stationary order: each input feeds all D accumulators in turn
+    // (operand reuse, D independent FMA chains instead of one serial chain)
+    C in[D], acc[D];
 #pragma unroll
     for (int j = 0; j < D; ++j) in[j] = v[base | deposit_mask<RB>(j, MASK)];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      C acc = czero<C>();
+    for (int i = 0; i < D; ++i) acc[i] = czero<C>();
 #pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if constexpr (kHoist) acc = cfma(M[i * D + j], in[j], acc);
-        else acc = cfma(Ms[i * D + j], in[j], acc);
+    for (int j = 0; j < D; ++j) {
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        if constexpr (kHoist) acc[i] = cfma(M[i * D + j], in[j], acc[i]);
+        else acc[i] = cfma(Ms[i * D + j], in[j], acc[i]);
       }
-      v[base | deposit_mask<RB>(i, MASK)] = acc;
     }
+#pragma unroll
+    for (int i = 0; i < D; ++i) v[base | deposit_mask<RB>(i, MASK)] = acc[i];
   }
 }
 
@@ -129,10 +133,129 @@ __device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, con
     reg_dense_op<C, RB>(v, op, pool);
 }
 
+// ------------------------------------------------ tensor-core GEMM phase
+// v <- U v for the 32 complex columns of each row, on mma.sync m16n8k16
+// (fp16 x fp16 -> fp32).  Layout (planner fuse_mma_phases): register index
+// rho = m | q0 << 3 | q1 << 4 holds complex column i = c + 4 m (c = lane & 3)
+// of warp row g + 8 q0 + 16 q1 (g = lane >> 2), i.e. exactly the A fragment of
+// the real block form [re im] and, for the outputs, the D fragment.  Each row
+// is scaled by a power of two s so that its largest component lies in
+// [2^14, 2^15), split x s = h + l in fp16 (round to nearest), and
+// D = h Bh + l Bh + h Bl accumulates in fp32 (relative error ~2^-22 of the
+// row's largest amplitude; Bh + Bl = the fp32 matrix to ~2^-22).
+__device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+  asm(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_half2(uint32_t x) {
+  float2 f;
+  asm("{\n .reg .f16 l, h;\n mov.b32 {l, h}, %2;\n cvt.f32.f16 %0, l;\n cvt.f32.f16 %1, h;\n}"
+      : "=f"(f.x), "=f"(f.y)
+      : "r"(x));
+  return f;
+}
+
+// The tensor cores' fp32 accumulation shrinks magnitudes systematically
+// (~1e-6 per phase measured); passes of unitary ops restore the tile's
+// 2-norm at the end (PassHeader::renorm, see k_reg_pass).
+__device__ __forceinline__ void mma_phase(float2 (&v)[32], const uint4* __restrict__ B, int lane) {
+  // per-row power-of-two scales (rows q = q0 | q1 << 1)
+  float sc[4], inv[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float mx = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float2 x = v[m | (q & 1) << 3 | (q >> 1) << 4];
+      mx = fmaxf(mx, fmaxf(fabsf(x.x), fabsf(x.y)));
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const int e = (__float_as_int(mx) >> 23) & 0xff;
+    const int se = min(max(268 - e, 1), 253);  // 2^(14 - exponent(mx)), clamped
+    sc[q] = __int_as_float(se << 23);
+    inv[q] = __int_as_float((254 - se) << 23);  // exact inverse
+  }
+  // A fragments [q1][kk][reg]: reg r -> m = 2 kk + (r >> 1), q0 = r & 1
+  uint32_t ah[2][4][4], al[2][4][4];
+#pragma unroll
+  for (int q1 = 0; q1 < 2; ++q1)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int q0 = r & 1, m = 2 * kk + (r >> 1);
+        const float s = sc[q0 | q1 << 1];
+        const float2 x = v[m | q0 << 3 | q1 << 4];
+        const float xr = x.x * s, xi = x.y * s;
+        const uint32_t hh = pack_half2(xr, xi);
+        const float2 hf = unpack_half2(hh);
+        ah[q1][kk][r] = hh;
+        al[q1][kk][r] = pack_half2(xr - hf.x, xi - hf.y);
+      }
+  // D = A B over 8 column tiles (nt = output m), two at a time
+#pragma unroll
+  for (int np = 0; np < 4; ++np) {
+    float d[2][2][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q1 = 0; q1 < 2; ++q1)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) d[a][q1][t] = 0.f;
+    // issue order: the 4 accumulators round-robin, so dependent HMMAs are 4
+    // instructions apart (hides the tensor-pipe latency at 2 warps/scheduler)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint4 b[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) b[a] = B[((2 * np + a) * 4 + kk) * 32 + lane];
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int q1 = 0; q1 < 2; ++q1) {
+            const uint32_t* A = t == 1 ? al[q1][kk] : ah[q1][kk];
+            const uint32_t b0 = t == 2 ? b[a].z : b[a].x, b1 = t == 2 ? b[a].w : b[a].y;
+            mma_f16(d[a][q1], A[0], A[1], A[2], A[3], b0, b1);
+          }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q1 = 0; q1 < 2; ++q1) {
+        const int m = 2 * np + a;
+        v[m | q1 << 4] = make_float2(d[a][q1][0] * inv[q1 << 1], d[a][q1][1] * inv[q1 << 1]);
+        v[m | 1 << 3 | q1 << 4] = make_float2(d[a][q1][2] * inv[1 | q1 << 1], d[a][q1][3] * inv[1 | q1 << 1]);
+      }
+  }
+}
+
+// 2-norm^2 of a thread's amplitudes, summed over its warp (in FP32).
+template <int NR>
+__device__ __forceinline__ float warp_norm2(const float2 (&v)[NR]) {
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) s = fmaf(v[r].x, v[r].x, fmaf(v[r].y, v[r].y, s));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 // Shared-memory layout of k_reg_pass: barriers | coefficient pool | thread
 // parts of the diagonal table indices | outside-tile parts (2S ring) | tiles.
 struct RegSmem {
-  size_t pool, dthr, dout, tiles, total;
+  size_t pool, dthr, dout, red, mats, tiles, total;
 };
 template <class C>
 __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
@@ -140,7 +263,9 @@ __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
   l.pool = 128;
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(C), 128);
   l.dout = l.dthr + align_up(size_t(h.n_ops) * kComputeThreads, 128);
-  l.tiles = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
+  l.red = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
+  l.mats = l.red + 128;  // [tile parity][start/end][warp] tile norms (renorm)
+  l.tiles = l.mats + (h.mma_phases ? size_t(h.tc_count) * kMmaMatBytes : 0);
   l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
   return l;
 }
@@ -154,13 +279,14 @@ template <class C, int RB>
 struct PhaseAddr {
   int base, sbase;
   int off[RB], soff[RB];
+  // ph.map: register-index bit i -> tile bit map[i]; thread bit b -> map[RB + b]
   __device__ __forceinline__ PhaseAddr(const PhaseDesc& ph, int tid) {
-    int b = tid;
+    int b = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b |= ((tid >> j) & 1) << ph.map[RB + j];
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
-      const int r = ph.R[i];
-      b = ((b >> r) << (r + 1)) | (b & ((1 << r) - 1));
-      off[i] = 1 << r;
+      off[i] = 1 << ph.map[i];
       soff[i] = Swz<C>::f(off[i]);
     }
     base = b;
@@ -220,6 +346,8 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
   C* pool = reinterpret_cast<C*>(smem + lay.pool);
   unsigned char* dthr = smem + lay.dthr;  // [op][tid]: thread part of each diagonal table index
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
+  const uint4* mats = reinterpret_cast<const uint4*>(smem + lay.mats);  // mma.sync B fragments
+  float* red = reinterpret_cast<float*>(smem + lay.red);
   C* tiles = reinterpret_cast<C*>(smem + lay.tiles);
   const int tid = threadIdx.x;
 
@@ -231,6 +359,11 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
     fence_mbar_init();
   }
   for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  if (h.mma_phases) {
+    const uint4* src = reinterpret_cast<const uint4*>(h.tc_mats);
+    uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);
+    for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += kThreads) dst[e] = src[e];
+  }
   for (int e = tid; e < h.n_ops * kComputeThreads; e += kThreads) {
     const OpDesc& op = args.ops[e / kComputeThreads];
     dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % kComputeThreads) : 0;
@@ -317,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
     const PhaseAddr<C, RB> la(lp, tid);
     last_g.gthr = global_of(la.base, h);
 #pragma unroll
-    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.R[i], h);
+    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.map[i], h);
   }
   int s = 0, xs = 0;
   uint32_t parity = 0;
@@ -356,6 +489,13 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
       if (last && !tout) mbar_arrive(&empty[s]);  // buffer free for the next load
+      if constexpr (sizeof(C) == 8 && RB == 5) {
+        if (p == 0 && h.renorm) {
+          const float w = warp_norm2(v);
+          if ((tid & 31) == 0) red[(it & 1) * 16 + (tid >> 5)] = w;
+        }
+        if (ph.flags & PH_MMA) mma_phase(v, mats + size_t(ph.tc) * (kMmaMatBytes / 16), tid & 31);
+      }
       for (int o = ph.op_begin; o < ph.op_end; ++o) {
         const OpDesc& op = args.ops[o];
         if (op.kind == OP_DIAG)
@@ -363,6 +503,27 @@ __global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __res
                           int(dthr[o * kComputeThreads + tid]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
         else
           reg_dense_op<C, RB>(v, op, pool);
+      }
+      if constexpr (sizeof(C) == 8 && RB == 5) {
+        if (last && h.renorm) {
+          // restore the tile's 2-norm (all ops of the pass are unitary)
+          const float w = warp_norm2(v);
+          float* rp = red + (it & 1) * 16;
+          if ((tid & 31) == 0) rp[8 + (tid >> 5)] = w;
+          compute_bar();
+          float n0 = 0.f, n1 = 0.f;
+#pragma unroll
+          for (int i = 0; i < kComputeWarps; ++i) {
+            n0 += rp[i];
+            n1 += rp[8 + i];
+          }
+          const float f = n1 > 0.f ? sqrtf(n0 / n1) : 1.f;
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            v[r].x *= f;
+            v[r].y *= f;
+          }
+        }
       }
       if (!last) {
 #pragma unroll

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
     const PhaseAddr<C, RB> la(lp, tid);
     last_g.gthr = global_of(la.base, h);
 #pragma unroll
-    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.R[i], h);
+    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.map[i], h);
   }
 
   int s = 0;

@@ -47,12 +47,17 @@ struct OpDesc {
 // OpDesc.srt[0..kt) = thread bits, OpDesc.tgt viewed as 32 bytes = the
 // register part of the table index for each rho).
 constexpr int kMaxPhases = 32;
-enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2 };
+enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2, PH_MMA = 4 };
 
 struct PhaseDesc {
   int op_begin, op_end, flags, tc;  // tc >= 0: tensor-core GEMM tc between [op_begin,op_mid) and [op_mid,op_end)
   int op_mid, pad0, pad1, pad2;
   int R[8];
+  // thread-local layout of the phase: map[i] = tile bit of register-index bit
+  // i (i < RB), map[RB + b] = tile bit of thread-index bit b.  Register-FMA
+  // phases: R ascending, then the other tile bits ascending.  mma.sync phases
+  // (PH_MMA) use the m16n8k16 fragment layout, see svb_regpass.cuh.
+  unsigned char map[16];
 };
 
 // k_tc_pass: fused phase matrices as TF32 hi/lo pairs in the K-major
@@ -60,6 +65,13 @@ struct PhaseDesc {
 // SBO 1024 B): [Ur_hi | Ui_hi | Ur_lo | Ui_lo], 32 x 32 fp32 each.
 constexpr int kTcMatBytes = 4 * 32 * 32 * 4;
 constexpr int kMaxTcPerPassDev = 2;
+
+// k_reg_pass mma.sync phases (c64, RB 5): the fused 32x32 complex phase
+// matrix as the real 64x64 block form B[k][n] (k = 2i + re/im of the input,
+// n = 2j + re/im of the output), split B = Bh + Bl in fp16 and stored in
+// m16n8k16 B-fragment order: [nt 0..7][kk 0..3][lane 0..31] x {bh0, bh1, bl0, bl1}.
+constexpr int kMmaMatBytes = 8 * 4 * 32 * 16;
+constexpr int kMaxMmaPerPass = 4;
 
 struct PassHeader {
   int T, L, m, n_ops;
@@ -80,9 +92,13 @@ struct PassHeader {
   // the non-tile bits in runs: origin = sum ((tile >> src) & (2^len-1)) << dst
   int n_gap_runs;
   int gap_src[kMaxHigh + 1], gap_dst[kMaxHigh + 1], gap_len[kMaxHigh + 1];
-  int tc_count;                 // fused GEMM matrices of this pass (k_tc_pass)
+  int tc_count;                 // fused GEMM matrices of this pass (k_tc_pass, or
+                                // k_reg_pass mma.sync phases when mma_phases)
   int has_outside;              // some diagonal op reads shard bits outside the tile
-  const float* tc_mats;         // device: tc_count * kTcMatBytes (set at launch)
+  const float* tc_mats;         // device: tc_count * kTcMatBytes / kMmaMatBytes (set at launch)
+  int mma_phases;               // k_reg_pass: tc_mats are mma.sync B fragments
+  int renorm;                   // k_reg_pass (c64 RB 5): every op is unitary -- restore
+                                // each tile's 2-norm at the end of the pass
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)

@@ -88,7 +88,8 @@ OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits"
         {"no_diag_merge": 1, "stages": 2}, {"stages": 4, "max_ops_per_pass": 1},
         {"no_reg_phases": 1}, {"reg_bits": 3, "tile_bits": 11}, {"cost_budget": -1.0, "stages": 2},
         {"reg_bits": 5, "tile_bits": 13, "cost_budget": 3.0, "tensor_cores": -1},
-        {"cost_budget": 6.0}, {"tensor_cores": -1, "no_window_search": 1}]
+        {"cost_budget": 6.0}, {"tensor_cores": -1, "no_window_search": 1},
+        {"tensor_cores": 2}, {"tensor_cores": 2, "tc_min_dense": 1, "cost_budget": 20.0}]
 
 
 @pytest.mark.parametrize("opts", OPTS, ids=[str(o) for o in OPTS])
@@ -96,6 +97,7 @@ OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits"
 def test_plan_shapes_vs_oracle(prec, opts):
     e = B200Engine("b200-opts", options=plan_options(**opts) if opts else None)
     for c in (fuse(gen.layered_circuit(14, layers=6, seed=1), 2)[0],
+              fuse(gen.layered_circuit(16, layers=8, seed=2), 2)[0],
               fuse(gen.qft_circuit(13), 2)[0],
               fuse(gen.layered_circuit(13, layers=4, seed=5), 3)[0],
               gen.random_su2_circuit(15, 90, seed=3)):

@@ -177,11 +177,18 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
             buf = amps[idx].copy()
             for ph in phases:
                 R = ph["R"][:rb]
-                nonr = [q for q in range(T) if q not in R]
+                mp = ph["map"]
+                assert sorted(mp[:T]) == list(range(T)), mp  # the layout is a bit permutation
+                if ph["mma"]:
+                    # fragment layout (svb_regpass.cuh mma_phase): K bits R[2..4] in
+                    # registers 0..2, R[0..1] in lanes 0..1; the GEMM acts on R
+                    assert mp[0:3] == R[2:5] and mp[5:7] == R[0:2], (mp, R)
+                    assert ph["op_begin"] == ph["op_end"]
+                    mp = list(R) + [q for q in range(T) if q not in R]
                 base = np.zeros(nthreads, dtype=np.int64)
-                for k, q in enumerate(nonr):
-                    base |= ((tid >> k) & 1) << q
-                loc = np.stack([base + sum(1 << R[i] for i in range(rb) if (rho >> i) & 1)
+                for k in range(T - rb):
+                    base |= ((tid >> k) & 1) << mp[rb + k]
+                loc = np.stack([base + sum(1 << mp[i] for i in range(rb) if (rho >> i) & 1)
                                 for rho in range(nr)], axis=1)
                 v = buf[loc]
                 order = list(range(ph["op_begin"], ph["op_mid"])) + ["tc"] + \
@@ -295,3 +302,33 @@ def test_diagonal_gates_outside_the_tile(prec):
     assert np.abs(got - want).max() <= (1e-12 if prec == "double" else 1e-5)
     f30, _ = fuse(gen.qft_circuit(30), 2)
     assert CircuitPlan(30, Precision.DOUBLE, f30.gates).num_passes <= 12
+
+
+MMA_CASES = [
+    ("layered14", lambda: fuse(gen.layered_circuit(14, layers=6, seed=3), 2)[0]),
+    ("layered13_w3", lambda: fuse(gen.layered_circuit(13, layers=4, seed=4), 3)[0]),
+    ("qft14", lambda: fuse(gen.qft_circuit(14), 2)[0]),
+    ("su2_14", lambda: gen.random_su2_circuit(14, 60, seed=9)),
+]
+
+
+@pytest.mark.parametrize("name,make", MMA_CASES, ids=[c[0] for c in MMA_CASES])
+def test_mma_phase_encoding(name, make):
+    """tensor_cores=2 (c64): whole register phases fused into one 32x32 matrix,
+    run by k_reg_pass as an mma.sync GEMM in the fragment layout."""
+    c = make()
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(c.num_qubits, Precision.SINGLE, c.gates, plan_options(tensor_cores=2))
+    infos = plan.passes()
+    assert all(i["reg_bits"] == 5 for i in infos)
+    got = emulate_reg(plan, c.num_qubits, "single")
+    assert np.abs(got - want).max() <= 1e-5
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+
+
+def test_mma_plans_layered28():
+    f, _ = fuse(gen.layered_circuit(28), 2)
+    plan = CircuitPlan(28, Precision.SINGLE, f.gates, plan_options(tensor_cores=2))
+    infos = plan.passes()
+    assert sum(i["num_tc"] for i in infos) > 0
+    assert sum(i["num_gates"] for i in infos) == 189
