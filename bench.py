@@ -145,8 +145,10 @@ def plan_kernels(plan) -> str:
     names = set()
     for p in range(plan.num_passes):
         info = plan.native.pass_info(p)
-        names.add("k_tc_pass" if info["num_tc"] else
-                  f"k_reg_pass<RB={info['reg_bits']}>" if info["reg_bits"] else "k_tile_pass")
+        mma = info["num_tc"] and any(plan.native.phase(p, f)["mma"] for f in range(info["num_phases"]))
+        names.add("k_tc_pass" if info["num_tc"] and not mma else
+                  f"k_reg_pass<RB={info['reg_bits']}>{'+mma.sync' if mma else ''}" if info["reg_bits"]
+                  else "k_tile_pass")
     return "+".join(sorted(names))
 
 
