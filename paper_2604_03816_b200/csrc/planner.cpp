@@ -265,6 +265,8 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
         const int kr = int(regb.size()), kt = int(thrb.size()), kx = int(extb.size());
         ro.mask = kt;  // stored in OpDesc.pad
         for (int j = 0; j < kt; ++j) ro.src[j] = thrb[j].first;
+        ro.rmask = 0;
+        for (int j = 0; j < kr; ++j) ro.rmask |= 1 << regb[j].first;
         ro.kx = kx;
         ro.xmask = 0;
         for (int j = 0; j < kx; ++j) ro.xmask |= 1ULL << extb[j].first;

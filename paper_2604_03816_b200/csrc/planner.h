@@ -57,6 +57,7 @@ struct RegOp {
   int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
   int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
   unsigned char rmap[32] = {0};  // diagonal: register part of the table index per rho
+  int rmask = 0;                  // diagonal: register indices the table reads (its kr bits)
   int kx = 0;                     // diagonal: top kx table bits are shard qubits outside the tile
   unsigned long long xmask = 0;   //   (ascending), selected per tile from the tile origin
   std::vector<cd> coeff;   // dense: matrix permuted to ascending register bits

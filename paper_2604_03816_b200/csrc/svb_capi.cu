@@ -151,6 +151,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
         std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
         d.kx = ro.kx;
+        d.rmask = ro.rmask;
         d.xmask = ro.xmask;
         if (ro.kx) a.h.has_outside = 1;
       }

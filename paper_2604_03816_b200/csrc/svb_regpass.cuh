@@ -99,12 +99,41 @@ __device__ __forceinline__ int diag_base(const OpDesc& op, int tid, long long or
   return diag_thread_part(op, tid) | diag_outside_part(op, origin);
 }
 
+// The table depends on the register index only through the bits in MASK: a
+// thread loads its 2^|MASK| factors once (table index = dbase | r << kt, r the
+// compact register part) and multiplies them in -- one shared-memory load per
+// distinct factor instead of one per amplitude.
+template <int RB, int MASK>
+__host__ __device__ constexpr int pext_c(int x) {
+  int r = 0, b = 0;
+  for (int i = 0; i < RB; ++i)
+    if ((MASK >> i) & 1) r |= ((x >> i) & 1) << b++;
+  return r;
+}
+template <class C, int RB, int MASK>
+__device__ __forceinline__ void reg_diag_mask(C (&v)[1 << RB], const C* __restrict__ table, int dbase, int kt) {
+  constexpr int K = popc_c(MASK);
+  C f[1 << K];
+#pragma unroll
+  for (int r = 0; r < (1 << K); ++r) f[r] = table[dbase | (r << kt)];
+#pragma unroll
+  for (int rho = 0; rho < (1 << RB); ++rho) v[rho] = cmul(v[rho], f[pext_c<RB, MASK>(rho)]);
+}
+
 template <class C, int RB>
 __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, const C* __restrict__ table, int dbase) {
-#pragma unroll
-  for (int rho = 0; rho < (1 << RB); ++rho) {
-    const int d = dbase | ((op.tgt[rho >> 2] >> (8 * (rho & 3))) & 0xff);
-    v[rho] = cmul(v[rho], table[d]);
+  switch (op.rmask) {
+#define SVB_DCASE(m) \
+  case m:            \
+    if constexpr ((m) < (1 << RB)) reg_diag_mask<C, RB, (m)>(v, table, dbase, op.pad); \
+    return;
+    SVB_DCASE(0) SVB_DCASE(1) SVB_DCASE(2) SVB_DCASE(3) SVB_DCASE(4) SVB_DCASE(5) SVB_DCASE(6) SVB_DCASE(7)
+    SVB_DCASE(8) SVB_DCASE(9) SVB_DCASE(10) SVB_DCASE(11) SVB_DCASE(12) SVB_DCASE(13) SVB_DCASE(14)
+    SVB_DCASE(15) SVB_DCASE(16) SVB_DCASE(17) SVB_DCASE(18) SVB_DCASE(19) SVB_DCASE(20) SVB_DCASE(21)
+    SVB_DCASE(22) SVB_DCASE(23) SVB_DCASE(24) SVB_DCASE(25) SVB_DCASE(26) SVB_DCASE(27) SVB_DCASE(28)
+    SVB_DCASE(29) SVB_DCASE(30) SVB_DCASE(31)
+#undef SVB_DCASE
+    default: break;
   }
 }
 

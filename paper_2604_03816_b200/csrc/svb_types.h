@@ -37,7 +37,7 @@ struct OpDesc {
   // diagonal gate never needs its qubits in the tile: its factor for those
   // bits is selected per tile from the tile origin.
   int kx;
-  int pad2;
+  int rmask;          // diagonal (register phases): register indices read by the table
   unsigned long long xmask;
 };
 
