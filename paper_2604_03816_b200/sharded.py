@@ -11,7 +11,10 @@ ref ``circuit.py:189-194``):
 
 * a *local segment* is every pending gate whose qubits are all local and that
   no deferred gate must precede (same dependency rule as the planner); it runs
-  as one planned sequence of tile passes on each shard;
+  as one planned sequence of tile passes on each shard.  Diagonal gates join
+  a segment even when they touch global qubits: a global bit is constant on a
+  rank, so each rank applies the diagonal restricted to its own global bits
+  (``localize``) -- diagonal gates never cause an exchange;
 * a *swap* brings the global qubits the next deferred gates need into the top
   m local positions: each rank splits its shard into 2^m contiguous blocks by
   those m bits and exchanges block w with the rank whose global bits equal w
@@ -76,6 +79,35 @@ def _physical_op(op, phys_of) -> GateOp:
     return GateOp(GateKind.CUSTOM, tuple(phys_of[t] for t in op.targets), (), effective_unitary(op))
 
 
+def _is_diagonal(op) -> bool:
+    u = effective_unitary(op)
+    return not np.any(u - np.diag(np.diag(u)))
+
+
+def localize(gates, n_local: int, rank: int) -> list:
+    """Specialise a local segment to one rank: a diagonal gate on physical
+    qubits >= n_local (global) keeps only its local qubits, its entries taken
+    at this rank's global bits; a diagonal on global qubits only becomes a
+    constant phase of the shard (a 1-qubit diagonal on qubit 0)."""
+    out = []
+    for op in gates:
+        tg = tuple(op.targets)
+        if all(t < n_local for t in tg):
+            out.append(op)
+            continue
+        d = np.diag(effective_unitary(op))
+        loc = [j for j, t in enumerate(tg) if t < n_local]
+        fixed = sum(((rank >> (t - n_local)) & 1) << j for j, t in enumerate(tg) if t >= n_local)
+        sub = np.empty(1 << len(loc), dtype=np.complex128)
+        for x in range(sub.size):
+            sub[x] = d[fixed | sum(((x >> k) & 1) << j for k, j in enumerate(loc))]
+        if loc:
+            out.append(GateOp(GateKind.CUSTOM, tuple(tg[j] for j in loc), (), np.diag(sub)))
+        else:
+            out.append(GateOp(GateKind.CUSTOM, (0,), (), np.diag([sub[0], sub[0]])))
+    return out
+
+
 def _schedule_once(gates, n: int, g: int, layout: list) -> tuple[Schedule, list]:
     nl = n - g
     phys_of = list(layout)
@@ -85,12 +117,13 @@ def _schedule_once(gates, n: int, g: int, layout: list) -> tuple[Schedule, list]
     sched = Schedule(n, g, list(layout), [])
     pending = list(range(len(gates)))
     first_victims: list = []
+    diag = [_is_diagonal(op) for op in gates]
     while pending:
         blocked: set = set()
         seg, deferred = [], []
         for i in pending:
             tg = gates[i].targets
-            if any(t in blocked for t in tg) or any(phys_of[t] >= nl for t in tg):
+            if any(t in blocked for t in tg) or (not diag[i] and any(phys_of[t] >= nl for t in tg)):
                 deferred.append(i)
                 blocked.update(tg)
             else:
@@ -271,7 +304,8 @@ class ShardedEngine:
         progs = []
         for st in sched.steps:
             if isinstance(st, LocalStep):
-                progs.append(("local", self.backend.plan(sched.n_local, precision, st.gates)))
+                gates = localize(st.gates, sched.n_local, self.rank)
+                progs.append(("local", self.backend.plan(sched.n_local, precision, gates)))
             else:
                 progs.append(("swap", st))
         return sched, progs

@@ -12,7 +12,7 @@ import torch
 
 from oracle import sv_oracle as orc
 from paper_2604_03816_b200.circuit import as_precision
-from paper_2604_03816_b200.sharded import LocalStep, SwapStep, block_peer, own_block, schedule, unpermute
+from paper_2604_03816_b200.sharded import LocalStep, SwapStep, block_peer, localize, own_block, schedule, unpermute
 
 _DT = {"single": torch.complex64, "double": torch.complex128}
 
@@ -60,8 +60,8 @@ def simulate(circuit, world: int, precision="double") -> np.ndarray:
               np.zeros(1 << nl, dtype=orc.dtype_of(precision)) for r in range(world)]
     for st in sched.steps:
         if isinstance(st, LocalStep):
-            for a in shards:
-                for op in st.gates:
+            for r, a in enumerate(shards):
+                for op in localize(st.gates, nl, r):
                     orc.apply_gate(a, nl, op)
         else:
             blk = 1 << (nl - st.m)
