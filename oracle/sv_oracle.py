@@ -147,6 +147,49 @@ def apply_gate(amps: np.ndarray, num_qubits: int, op) -> np.ndarray:
     return amps
 
 
+def _group_offsets_range(n: int, targets, g0: int, g1: int) -> list[np.ndarray]:
+    # _group_offsets restricted to groups [g0, g1) (ref engines.py:94-105)
+    q = len(targets)
+    base = np.arange(g0, g1, dtype=np.intp)
+    for t in sorted(targets):
+        base = ((base >> t) << (t + 1)) | (base & ((1 << t) - 1))
+    return [base + sum(1 << targets[b] for b in range(q) if (j >> b) & 1)
+            for j in range(1 << q)]
+
+
+def apply_gate_parallel(amps: np.ndarray, num_qubits: int, op, pool, workers: int) -> np.ndarray:
+    """The reference's chunked data-parallel kernels (ref ParallelEngine,
+    engines.py:206-262) generalised from 2 to `workers` chunks: contiguous
+    slices of the pair views / of the group range, each run by the reference
+    kernel on a pool thread (numpy releases the GIL).  Element-wise the same
+    arithmetic as apply_gate, hence bit-identical results (as
+    ref test_engines.py:105-117 pins for the 2-chunk engine)."""
+    tg = tuple(int(t) for t in op.targets)
+    if any(not 0 <= t < num_qubits for t in tg):
+        raise ValueError(f"target out of range for {num_qubits} qubits: {tg}")
+    u = gate_unitary(op).astype(amps.dtype)
+    if workers < 2 or amps.size < (1 << 16):
+        return apply_gate(amps, num_qubits, op)
+    if len(tg) == 1:
+        a, b = _pair_halves(amps, tg[0])
+        ax = 0 if (a.ndim == 1 or a.shape[0] >= workers) else 1
+        n = a.shape[ax]
+        cuts = [n * w // workers for w in range(workers + 1)]
+        sl = [(slice(cuts[w], cuts[w + 1]),) if ax == 0 else (slice(None), slice(cuts[w], cuts[w + 1]))
+              for w in range(workers)]
+        futs = [pool.submit(_butterfly, a[x], b[x], u) for x in sl]
+    else:
+        groups = amps.size >> len(tg)
+        cuts = [groups * w // workers for w in range(workers + 1)]
+
+        def chunk(g0, g1):
+            _group_apply(amps, u, _group_offsets_range(num_qubits, tg, g0, g1))
+        futs = [pool.submit(chunk, cuts[w], cuts[w + 1]) for w in range(workers)]
+    for f in futs:
+        f.result()
+    return amps
+
+
 def apply_matrix(amps: np.ndarray, num_qubits: int, targets, u: np.ndarray) -> np.ndarray:
     """Apply an explicit 2^k x 2^k matrix with the reference kernels."""
     class _Op:  # minimal CUSTOM op

@@ -104,3 +104,20 @@ def test_oracle_bit_exact_vs_live_reference():
             want = ref.run_circuit(rcirc, prec).amplitudes
             got = orc.run_circuit(c, prec.value)
             assert np.array_equal(got, want)
+
+
+def test_parallel_port_is_bit_identical():
+    """The threaded port (ref ParallelEngine generalised to N chunks) used by
+    bench.py's CPU legs reproduces the serial oracle bit for bit."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2604_03816_b200 import generators as gen
+    from paper_2604_03816_b200.fusion import fuse
+    for c, prec in ((fuse(gen.layered_circuit(17, layers=3), 2)[0], "single"),
+                    (gen.qft_circuit(16), "double"),
+                    (fuse(gen.layered_circuit(16, layers=2, seed=3), 3)[0], "double")):
+        want = orc.run_circuit(c, prec)
+        got = orc.init_state(c.num_qubits, prec)
+        with ThreadPoolExecutor(4) as pool:
+            for op in c.gates:
+                orc.apply_gate_parallel(got, c.num_qubits, op, pool, 4)
+        assert np.array_equal(got, want)
