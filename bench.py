@@ -402,7 +402,7 @@ def run_b200(args):
                                          "the passes are HBM- or FMA-bound, whichever is larger"}},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8 + (8 if pc == 0 else 16),
-                "path": "B200Engine.run_circuit(fused circuit) + norm_squared + amplitude[0] read"},
+                "path": "B200Engine.run_circuit(fused circuit; plan cached by content after the first, untimed call) + norm_squared + amplitude[0] read"},
         "gpu_launches": args.steps * (n_passes + 2),
         "clocks": clk_summary,
         "cpu_baseline": cpu,

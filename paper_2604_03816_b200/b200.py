@@ -69,11 +69,11 @@ def plan_options(**kw) -> _native.PlanOptions:
 class CircuitPlan:
     """A lowered circuit: the native plan plus bookkeeping for reports."""
 
-    def __init__(self, num_qubits: int, precision, gates, options=None, qubit_map=None):
+    def __init__(self, num_qubits: int, precision, gates, options=None, qubit_map=None, lowered=None):
         self.num_qubits = num_qubits
         self.precision = as_precision(precision)
         self.num_gates = len(gates)
-        ks, tg, mats = lower_gates(gates, qubit_map)
+        ks, tg, mats = lowered if lowered is not None else lower_gates(gates, qubit_map)
         self.native = _native.NativePlan(num_qubits, prec_code(self.precision), ks, tg, mats, options)
 
     @property
@@ -215,9 +215,29 @@ class B200Engine(EngineBase):
         self._apply(state, np.asarray(u), tuple(int(t) for t in targets))
 
     def plan(self, circuit, precision=Precision.DOUBLE, options=None) -> CircuitPlan:
-        """Lower a (fused) circuit into tile passes (host-only, no GPU work)."""
-        return CircuitPlan(circuit.num_qubits, precision, list(circuit.gates),
-                           options if options is not None else self.options)
+        """Lower a (fused) circuit into tile passes (host-only, no GPU work).
+
+        Plans are cached per engine by content (qubit count, precision, gate
+        arities / targets / matrices, options): running the same circuit again
+        -- the serving case -- skips the planner."""
+        import hashlib
+        opts = options if options is not None else self.options
+        gates = list(circuit.gates)
+        lowered = lower_gates(gates)
+        h = hashlib.blake2b(digest_size=20)
+        for arr in lowered:
+            h.update(np.ascontiguousarray(arr).tobytes())
+        if opts is not None:
+            h.update(bytes(opts))
+        key = (circuit.num_qubits, as_precision(precision).value, h.digest())
+        cache = self.__dict__.setdefault("_plans", {})
+        plan = cache.get(key)
+        if plan is None:
+            plan = CircuitPlan(circuit.num_qubits, precision, gates, opts, lowered=lowered)
+            if len(cache) >= 16:
+                cache.pop(next(iter(cache)))
+            cache[key] = plan
+        return plan
 
     def execute(self, state: DeviceStateVector, plan: CircuitPlan) -> DeviceStateVector:
         if plan.num_qubits != state.num_qubits:
