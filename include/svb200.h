@@ -49,7 +49,7 @@ typedef struct svb_plan svb_plan;
 
 /* Planner knobs; zero-initialise for defaults. */
 typedef struct svb_plan_options {
-  int tile_bits;        /* qubits per shared-memory tile (0: 13 for c64, 11 for c128) */
+  int tile_bits;        /* qubits per shared-memory tile (0: 13 for c64, 12 for c128) */
   int min_low_bits;     /* contiguous low qubits always in the tile (0: 512-B chunks) */
   int max_ops_per_pass; /* 0: 48 (kernel limit)                                      */
   double cost_budget;   /* modelled compute per pass as a multiple of the pass's HBM
@@ -57,7 +57,7 @@ typedef struct svb_plan_options {
   int no_diag_merge;    /* 1: do not merge diagonal runs into one table              */
   int stages;           /* TMA pipeline depth per CTA (0: deepest ring that keeps the
                            CTAs per SM of a 2-stage ring)                         */
-  int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 3 c128) */
+  int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 4 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
   int tensor_cores;     /* c64 only: 2 = fuse whole register phases into warp-level
                            tensor-core GEMMs (mma.sync f16 hi/lo, in k_reg_pass);

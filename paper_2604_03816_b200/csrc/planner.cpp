@@ -15,9 +15,12 @@ constexpr int kMaxTcPerPass = 2;        // fused GEMM matrices per pass (shared 
 constexpr double kTcDenseCost = 0.15;   // planner cost of a dense gate in a tensor-core pass
 constexpr double kTcDefaultBudget = 3.0;
 
-int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 11; }
+// c128: 12-qubit tiles with 16 amplitudes per thread at 1 CTA/SM (measured
+// layered-30 450 ms vs 513 ms for 11-qubit tiles x 8 amplitudes at 2 CTAs/SM:
+// 4 register bits hold ~3 brickwork gates per phase instead of ~2)
+int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 12; }
 int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
-int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 3; }
+int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 4; }
 double default_cost_budget(int prec) { return prec == SVB_C64 ? 7.0 : 5.0; }
 // tile = RB + 8 qubits for the register kernel
 
@@ -153,9 +156,61 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   std::vector<int> pending(p.ops.size());
   for (size_t i = 0; i < p.ops.size(); ++i) pending[i] = int(i);
   std::vector<std::vector<int>> sets, members;
+  // dense ops a phase with register set `mask` (tile bits) would absorb
+  auto absorbed = [&](const std::vector<int>& pend, int mask) {
+    int dense = 0, all_block = 0, dense_block = 0;
+    for (int i : pend) {
+      const KernelOp& op = p.ops[i];
+      int bits = 0;
+      for (int j = 0; j < op.k; ++j)
+        if (op.tgt[j] < p.T) bits |= 1 << op.tgt[j];
+      const bool blocked = (bits & all_block) || (op.kind == OP_DENSE && (bits & dense_block));
+      const bool take = !blocked && (op.kind == OP_DIAG || (bits & ~mask) == 0);
+      if (take) {
+        dense += op.kind == OP_DENSE;
+      } else {
+        (op.kind == OP_DIAG ? dense_block : all_block) |= bits;
+      }
+    }
+    return dense;
+  };
   while (!pending.empty()) {
     std::vector<char> block_all(p.T, 0), block_dense(p.T, 0);
     std::vector<int> R, took, rest;
+    // Register set: the RB tile bits that absorb the most dense ops (exhaustive
+    // over the bits the pending dense ops touch; fewer phases = fewer
+    // transposes, and a tensor-core phase costs the same whatever it holds).
+    // First-fit order decides only when fewer than RB bits are in play.
+    int cand = 0;
+    for (int i : pending)
+      if (p.ops[i].kind == OP_DENSE)
+        for (int j = 0; j < p.ops[i].k; ++j) cand |= 1 << p.ops[i].tgt[j];
+    int fixed = -1;
+    if (__builtin_popcount(cand) > RB && __builtin_popcount(cand) <= 16) {
+      std::vector<int> cb;
+      for (int b = 0; b < p.T; ++b)
+        if ((cand >> b) & 1) cb.push_back(b);
+      const int nb = int(cb.size());
+      int best = -1;
+      std::vector<int> sel(RB);
+      for (int i = 0; i < RB; ++i) sel[i] = i;
+      while (true) {  // all RB-subsets of cb, lexicographic
+        int mask = 0;
+        for (int i = 0; i < RB; ++i) mask |= 1 << cb[sel[i]];
+        const int got = absorbed(pending, mask);
+        if (got > best) {
+          best = got;
+          fixed = mask;
+        }
+        int i = RB - 1;
+        while (i >= 0 && sel[i] == nb - RB + i) --i;
+        if (i < 0) break;
+        ++sel[i];
+        for (int j = i + 1; j < RB; ++j) sel[j] = sel[j - 1] + 1;
+      }
+      for (int b = 0; b < p.T; ++b)
+        if ((fixed >> b) & 1) R.push_back(b);
+    }
     for (int i : pending) {
       const KernelOp& op = p.ops[i];
       bool blocked = false;
@@ -166,6 +221,9 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       if (!blocked) {
         if (op.kind == OP_DIAG) {
           take = true;
+        } else if (fixed >= 0) {
+          take = true;
+          for (int j = 0; j < op.k; ++j) take = take && ((fixed >> op.tgt[j]) & 1);
         } else {
           std::vector<int> u = R;
           for (int j = 0; j < op.k; ++j)

@@ -363,7 +363,7 @@ struct GlobalAddr {
 };
 
 template <class C, int RB>
-__global__ void __launch_bounds__(kThreads, RB >= 5 ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+__global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + 8;
   constexpr int NR = 1 << RB;
   extern __shared__ __align__(1024) unsigned char smem[];
