@@ -147,7 +147,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   // instantiated register kernels: c64 RB 3..5, c128 RB 3..4 (8 thread bits);
   // the tensor-core kernel: c64 RB 5 with 7 thread bits
   if (TB == 8 && (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4))) return false;
-  if (TB == 7 && (RB != 5 || prec != SVB_C64)) return false;
+  if (TB == 7 && (RB != 5 || prec != SVB_C64)) return false;  // k_tc_pass / k_reg_pass<float2, 5, 7>
   if (p.T != RB + TB) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
@@ -486,7 +486,8 @@ void fuse_tc_phases(Pass& p, int min_dense, int max_tc) {
 // of the rows g, g + 8, g + 16, g + 24 (register bits 3, 4) of its warp.
 void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
   const int RB = p.reg_bits;
-  if (RB != 5 || p.thread_bits != 8 || prec != SVB_C64) return;
+  const int TB = p.thread_bits;
+  if (RB != 5 || (TB != 8 && TB != 7) || prec != SVB_C64) return;
   const int D = 1 << RB;
   struct Cand { int dense, phase; };
   std::vector<Cand> cands;
@@ -560,8 +561,10 @@ void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
         take_row(best);
       }
       take_row(std::find(rows.begin(), rows.end(), 4) != rows.end() ? 4 : rows[0]);
+      // warp bits: the remaining rows (3 with one tile stream, 2 with two)
       const int lay[13] = {ph.R[2], ph.R[3], ph.R[4], rows[0], rows[1],
-                           ph.R[0], ph.R[1], pick[0], pick[1], pick[2], rows[2], rows[3], rows[4]};
+                           ph.R[0], ph.R[1], pick[0], pick[1], pick[2], rows[2], rows[3],
+                           TB == 8 ? rows[4] : 0};
       for (int i = 0; i < 13; ++i) ph.map[i] = lay[i];
       set_layout_flags(ph, RB, prec, f == 0, f + 1 == int(p.phases.size()));
     } else {
@@ -976,6 +979,9 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     p.num_gates = int(taken.size());
     if (use_tc && p.T == 12 && build_phases(p, 5, prec, 7)) {
       fuse_tc_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxTcPerPass);
+    } else if (use_mma && p.T == 12 && build_phases(p, 5, prec, 7)) {
+      // 12-qubit tiles: two warp groups with their own tile streams (k_reg_pass TB 7)
+      fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile

@@ -70,6 +70,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
                          (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
+                         (const void*)k_reg_pass<float2, 5, 7>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -124,6 +125,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.reg_bits = p.reg_bits;
   a.h.tc_count = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
   a.h.mma_phases = p.mma_phases ? 1 : 0;
+  a.h.thread_bits = p.phases.empty() ? 8 : p.thread_bits;
   a.h.renorm = p.renorm ? 1 : 0;
   a.h.tc_mats = nullptr;
   int off = 0;
@@ -274,9 +276,14 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   if (a.h.n_phases > 0) {
     if constexpr (sizeof(C) == 8) {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 5) return fail(SVB_EUNSUPPORTED, "c64 reg_bits must be 3..5");
-      fn = a.h.reg_bits == 5 ? k_reg_pass<C, 5> : a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
+      if (a.h.thread_bits == 7 && a.h.reg_bits != 5) return fail(SVB_EUNSUPPORTED, "two-stream tiles need reg_bits 5");
+      fn = a.h.thread_bits == 7 ? k_reg_pass<C, 5, 7>
+           : a.h.reg_bits == 5  ? k_reg_pass<C, 5>
+           : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
+                                : k_reg_pass<C, 3>;
     } else {
-      if (a.h.reg_bits < 3 || a.h.reg_bits > 4) return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4");
+      if (a.h.reg_bits < 3 || a.h.reg_bits > 4 || a.h.thread_bits != 8)
+        return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4 (8 thread bits)");
       fn = a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
     }
   } else {
@@ -303,8 +310,10 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
       }
     }
   }
-  // deepest TMA ring that fits the opt-in shared memory (>= 2 stages)
+  // deepest TMA ring that fits the opt-in shared memory (>= 2 stages); two
+  // tile streams (7 thread bits) own alternate stages, so the ring is even
   while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
+  if (a.h.n_phases > 0 && a.h.thread_bits == 7 && (a.h.stages & 1)) --a.h.stages;
   const size_t smem = smem_of();
   int per_sm = 0;
   SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));

@@ -291,9 +291,9 @@ __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
   RegSmem l;
   l.pool = 128;
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(C), 128);
-  l.dout = l.dthr + align_up(size_t(h.n_ops) * kComputeThreads, 128);
+  l.dout = l.dthr + align_up(size_t(h.n_ops) * (size_t(1) << h.thread_bits), 128);
   l.red = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
-  l.mats = l.red + 128;  // [tile parity][start/end][warp] tile norms (renorm)
+  l.mats = l.red + 256;  // [group][tile parity][start/end][warp] tile norms (renorm)
   l.tiles = l.mats + (h.mma_phases ? size_t(h.tc_count) * kMmaMatBytes : 0);
   l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
   return l;
@@ -362,18 +362,34 @@ struct GlobalAddr {
   }
 };
 
-template <class C, int RB>
+// TB = thread bits of a tile: 8 -- the 8 compute warps share one tile stream;
+// 7 -- two groups of 4 warps, each with its own tile stream (tiles alternate
+// between the groups) and its own named barrier, so one group's shared-memory
+// transposes and conversions overlap the other's tensor-core work.
+template <int G>
+__device__ __forceinline__ void group_bar(int group) {
+  if constexpr (G == 1) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(kComputeThreads / G) : "memory");
+  }
+}
+
+template <class C, int RB, int TB = 8>
 __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
-  constexpr int T = RB + 8;
+  constexpr int T = RB + TB;
   constexpr int NR = 1 << RB;
+  constexpr int NTG = 1 << TB;                 // threads per tile stream
+  constexpr int NG = kComputeThreads / NTG;    // tile streams (warp groups)
+  constexpr int WPG = NTG / 32;                // warps per group
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const int S = h.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // tile landed (1 arrival + tx bytes)
-  uint64_t* empty = full + S;                           // tile buffer drained (256 arrivals)
+  uint64_t* empty = full + S;                           // tile buffer drained (NTG arrivals)
   const RegSmem lay = reg_smem_layout<C>(h);
   C* pool = reinterpret_cast<C*>(smem + lay.pool);
-  unsigned char* dthr = smem + lay.dthr;  // [op][tid]: thread part of each diagonal table index
+  unsigned char* dthr = smem + lay.dthr;  // [op][thread]: thread part of each diagonal table index
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
   const uint4* mats = reinterpret_cast<const uint4*>(smem + lay.mats);  // mma.sync B fragments
   float* red = reinterpret_cast<float*>(smem + lay.red);
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kComputeThreads);
+      mbar_init(&empty[s], NTG);
     }
     fence_mbar_init();
   }
@@ -393,9 +409,9 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
     uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);
     for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += kThreads) dst[e] = src[e];
   }
-  for (int e = tid; e < h.n_ops * kComputeThreads; e += kThreads) {
-    const OpDesc& op = args.ops[e / kComputeThreads];
-    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % kComputeThreads) : 0;
+  for (int e = tid; e < h.n_ops * NTG; e += kThreads) {
+    const OpDesc& op = args.ops[e / NTG];
+    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
   }
   __syncthreads();
   // outside-tile table bits of tile `it` (written by the producer before it
@@ -466,54 +482,58 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   }
 
   // -------------------------------------------------------- compute threads
+  const int group = NG == 1 ? 0 : tid / NTG;
+  const int gt = tid & (NTG - 1);  // thread index within the tile stream
   const int np = h.n_phases;
-  // per-thread global offset of the linear layout x = rho * 256 + tid
+  // per-thread global offset of the linear layout x = rho * NTG + gt
   GlobalAddr<RB> lin_g;
-  lin_g.gthr = global_of(tid, h);
+  lin_g.gthr = global_of(gt, h);
 #pragma unroll
-  for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(8 + i, h);
+  for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(TB + i, h);
   // global addressing of the last phase's direct store is tile-invariant
   GlobalAddr<RB> last_g;
   {
     const PhaseDesc& lp = args.phases[np - 1];
-    const PhaseAddr<C, RB> la(lp, tid);
+    const PhaseAddr<C, RB> la(lp, gt);
     last_g.gthr = global_of(la.base, h);
 #pragma unroll
     for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.map[i], h);
   }
-  int s = 0, xs = 0;
+  // stage / barrier parity / outside-index slot / renorm slot of tile `it`,
+  // advanced incrementally (S is even when NG == 2)
+  int s = group, xs = group, tpar = 0;
   uint32_t parity = 0;
-  for (long long it = 0; it < mine;
-       ++it, (++s == S ? (s = 0, parity ^= 1) : 0), xs = xs + 1 == 2 * S ? 0 : xs + 1) {
+  for (long long it = group; it < mine; it += NG) {
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
     const long long origin = tile_base(tile, h);
+    float* rp = red + (group * 2 + tpar) * 16;  // renorm partials of this tile
     mbar_wait(&full[s], parity);
     C v[NR];
     for (int p = 0; p < np; ++p) {
       const PhaseDesc& ph = args.phases[p];
-      const PhaseAddr<C, RB> a(ph, tid);
+      const PhaseAddr<C, RB> a(ph, gt);
       const bool last = p == np - 1;
       const bool tout = last && (ph.flags & PH_TRANSPOSE_OUT);
       if (p == 0) {
         if (ph.flags & PH_TRANSPOSE_IN) {
           // linear (TMA) layout -> swizzled layout through conflict-free reads
 #pragma unroll
-          for (int r = 0; r < NR; ++r) v[r] = buf[r * kComputeThreads + tid];
-          compute_bar();
+          for (int r = 0; r < NR; ++r) v[r] = buf[r * NTG + gt];
+          group_bar<NG>(group);
 #pragma unroll
-          for (int r = 0; r < NR; ++r) buf[Swz<C>::f(r * kComputeThreads + tid)] = v[r];
-          compute_bar();
+          for (int r = 0; r < NR; ++r) buf[Swz<C>::f(r * NTG + gt)] = v[r];
+          group_bar<NG>(group);
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
         } else {
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[a.lin(r)];
           // all reads of the linear layout finish before swizzled writes
-          if (np > 1 || tout) compute_bar();
+          if (np > 1 || tout) group_bar<NG>(group);
         }
       } else {
-        compute_bar();
+        group_bar<NG>(group);
 #pragma unroll
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
@@ -521,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
       if constexpr (sizeof(C) == 8 && RB == 5) {
         if (p == 0 && h.renorm) {
           const float w = warp_norm2(v);
-          if ((tid & 31) == 0) red[(it & 1) * 16 + (tid >> 5)] = w;
+          if ((gt & 31) == 0) rp[gt >> 5] = w;
         }
         if (ph.flags & PH_MMA) mma_phase(v, mats + size_t(ph.tc) * (kMmaMatBytes / 16), tid & 31);
       }
@@ -529,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         const OpDesc& op = args.ops[o];
         if (op.kind == OP_DIAG)
           reg_diag<C, RB>(v, op, pool + op.coeff_off,
-                          int(dthr[o * kComputeThreads + tid]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
+                          int(dthr[o * NTG + gt]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
         else
           reg_dense_op<C, RB>(v, op, pool);
       }
@@ -537,12 +557,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         if (last && h.renorm) {
           // restore the tile's 2-norm (all ops of the pass are unitary)
           const float w = warp_norm2(v);
-          float* rp = red + (it & 1) * 16;
-          if ((tid & 31) == 0) rp[8 + (tid >> 5)] = w;
-          compute_bar();
+          if ((gt & 31) == 0) rp[8 + (gt >> 5)] = w;
+          group_bar<NG>(group);
           float n0 = 0.f, n1 = 0.f;
 #pragma unroll
-          for (int i = 0; i < kComputeWarps; ++i) {
+          for (int i = 0; i < WPG; ++i) {
             n0 += rp[i];
             n1 += rp[8 + i];
           }
@@ -558,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
       } else if (!tout) {
-        // direct store from registers (coalesced: R avoids the bank-row bits)
+        // direct store from registers (coalesced: the lanes cover the bank-row bits)
         C* __restrict__ dst = amps + origin + last_g.gthr;
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[last_g.at(r) - last_g.gthr] = v[r];
@@ -566,13 +585,21 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         // swizzled smem, then contiguous reads -> coalesced global stores
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
-        compute_bar();
+        group_bar<NG>(group);
         C* __restrict__ dst = amps + origin;
 #pragma unroll
-        for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * kComputeThreads + tid)];
+        for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * NTG + gt)];
         mbar_arrive(&empty[s]);
       }
     }
+    s += NG;
+    if (s >= S) {
+      s -= S;
+      parity ^= 1;
+    }
+    xs += NG;
+    if (xs >= 2 * S) xs -= 2 * S;
+    tpar ^= 1;
   }
 }
 
