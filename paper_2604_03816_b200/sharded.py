@@ -351,6 +351,13 @@ class ShardedEngine:
         if not peers:
             return
         npeer = len(peers)
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            # gloo moves host tensors only (used by the single-GPU multi-process
+            # tests): stage each block through host memory
+            self._exchange_via_host(t, blk, mine, peers)
+            if hasattr(state, "touch"):
+                state.touch()
+            return
         stage = self._staging_for(t, 2 * npeer * chunk).view(2, npeer, chunk)
 
         def issue(c):
@@ -371,6 +378,26 @@ class ShardedEngine:
             inflight = nxt
         if hasattr(state, "touch"):
             state.touch()
+
+
+    def _exchange_via_host(self, t, blk: int, mine: int, peers):
+        dist = self.dist
+        ops, recv = [], []
+        for w, peer in peers:
+            src = t[w * blk:(w + 1) * blk].cpu()
+            buf = torch_empty_like_host(src)
+            ops.append(dist.P2POp(dist.isend, src, peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            recv.append((w, buf))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        for w, buf in recv:
+            t[w * blk:(w + 1) * blk].copy_(buf)
+
+
+def torch_empty_like_host(x):
+    import torch
+    return torch.empty_like(x, device="cpu")
 
 
 class ShardedState:

@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
-rm -f gpurun_out/sweep.txt
-for a in "" "--tile-bits 12" "--tile-bits 12 --stages 4" "--tile-bits 12 --cost-budget 12" "--config qft30" "--config layered-30 --precision double"; do
-  echo "ARGS $a :: $(timeout 400 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>&1 | tail -1)" >> gpurun_out/sweep.txt
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 300 -k "sharded or qft18" > gpurun_out/pt_new.txt 2>&1; echo "rc=$?" >> gpurun_out/pt_new.txt
