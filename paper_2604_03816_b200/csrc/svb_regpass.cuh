@@ -485,20 +485,9 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   const int group = NG == 1 ? 0 : tid / NTG;
   const int gt = tid & (NTG - 1);  // thread index within the tile stream
   const int np = h.n_phases;
-  // per-thread global offset of the linear layout x = rho * NTG + gt
-  GlobalAddr<RB> lin_g;
-  lin_g.gthr = global_of(gt, h);
-#pragma unroll
-  for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(TB + i, h);
-  // global addressing of the last phase's direct store is tile-invariant
-  GlobalAddr<RB> last_g;
-  {
-    const PhaseDesc& lp = args.phases[np - 1];
-    const PhaseAddr<C, RB> la(lp, gt);
-    last_g.gthr = global_of(la.base, h);
-#pragma unroll
-    for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(lp.map[i], h);
-  }
+  // global addressing of the stores (tile-invariant) is rebuilt at the store
+  // from the pass description: keeping 2 x RB 64-bit offsets live across the
+  // tile loop would cost ~24 registers the tensor-core phases need
   // stage / barrier parity / outside-index slot / renorm slot of tile `it`,
   // advanced incrementally (S is even when NG == 2)
   int s = group, xs = group, tpar = 0;
@@ -578,6 +567,10 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
       } else if (!tout) {
         // direct store from registers (coalesced: the lanes cover the bank-row bits)
+        GlobalAddr<RB> last_g;
+        last_g.gthr = global_of(a.base, h);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) last_g.goff[i] = 1LL << gpos(ph.map[i], h);
         C* __restrict__ dst = amps + origin + last_g.gthr;
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[last_g.at(r) - last_g.gthr] = v[r];
@@ -586,6 +579,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
         group_bar<NG>(group);
+        // per-thread global offset of the linear layout x = rho * NTG + gt
+        GlobalAddr<RB> lin_g;
+        lin_g.gthr = global_of(gt, h);
+#pragma unroll
+        for (int i = 0; i < RB; ++i) lin_g.goff[i] = 1LL << gpos(TB + i, h);
         C* __restrict__ dst = amps + origin;
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * NTG + gt)];

@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 300 -k "sharded or qft18" > gpurun_out/pt_new.txt 2>&1; echo "rc=$?" >> gpurun_out/pt_new.txt
+rm -f gpurun_out/sweep.txt
+for a in "" "--config qft30" "--config layered-30 --precision double" "--tensor-cores -1"; do
+  echo "ARGS $a :: $(timeout 400 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>&1 | tail -1)" >> gpurun_out/sweep.txt
+done
+timeout 500 python tools/probe_phase.py SINGLE > gpurun_out/probe_phase_mma.txt 2>&1
