@@ -146,8 +146,10 @@ def plan_kernels(plan) -> str:
     for p in range(plan.num_passes):
         info = plan.native.pass_info(p)
         mma = info["num_tc"] and any(plan.native.phase(p, f)["mma"] for f in range(info["num_phases"]))
+        tb = info["tile_bits"] - info["reg_bits"]
+        tcn = ("+tcgen05" if tb == 7 else "+mma.sync") if mma else ""
         names.add("k_tc_pass" if info["num_tc"] and not mma else
-                  f"k_reg_pass<RB={info['reg_bits']}>{'+mma.sync' if mma else ''}" if info["reg_bits"]
+                  f"k_reg_pass<RB={info['reg_bits']},TB={tb}>{tcn}" if info["reg_bits"]
                   else "k_tile_pass")
     return "+".join(sorted(names))
 

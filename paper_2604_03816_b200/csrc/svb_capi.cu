@@ -380,6 +380,30 @@ void pack_mma(const std::vector<cd>& U, std::vector<float>& out) {
       }
 }
 
+// tcgen05 (kind::f16, K-major, SWIZZLE_NONE) B operand of the same block form:
+// [Bh | Bl], 64 (n) x 64 (k) fp16 each, byte offset
+// (n / 8) 1024 + (k / 8) 128 + (n % 8) 16 + (k % 8) 2.
+void pack_t5(const std::vector<cd>& U, std::vector<float>& out) {
+  auto Bv = [&](int k, int n) -> double {
+    const int i = k >> 1, a = k & 1, j = n >> 1, b = n & 1;
+    const cd u = U[size_t(j) * 32 + i];
+    if (a == 0) return b == 0 ? u.real() : u.imag();
+    return b == 0 ? -u.imag() : u.real();
+  };
+  const size_t base = out.size();
+  out.resize(base + kMmaMatBytes / 4);
+  unsigned char* w = reinterpret_cast<unsigned char*>(out.data() + base);
+  for (int n = 0; n < 64; ++n)
+    for (int k = 0; k < 64; ++k) {
+      const float f = float(Bv(k, n));
+      const __half hh = __float2half_rn(f);
+      const __half ll = __float2half_rn(f - __half2float(hh));
+      const size_t off = size_t(n / 8) * 1024 + size_t(k / 8) * 128 + size_t(n % 8) * 16 + size_t(k % 8) * 2;
+      std::memcpy(w + off, &hh, 2);
+      std::memcpy(w + 8192 + off, &ll, 2);
+    }
+}
+
 void pack_tc(svb_plan* p) {
   p->tc_host.clear();
   p->tc_offset.assign(p->plan.passes.size(), 0);
@@ -387,7 +411,12 @@ void pack_tc(svb_plan* p) {
     const Pass& ps = p->plan.passes[i];
     p->tc_offset[i] = p->tc_host.size();
     if (ps.mma_phases) {
-      for (const auto& U : ps.tc_mats) pack_mma(U, p->tc_host);
+      for (const auto& U : ps.tc_mats) {
+        if (ps.thread_bits == 7)
+          pack_t5(U, p->tc_host);
+        else
+          pack_mma(U, p->tc_host);
+      }
       continue;
     }
     if (!ps.tensor_cores) continue;

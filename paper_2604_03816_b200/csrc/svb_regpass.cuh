@@ -281,6 +281,139 @@ __device__ __forceinline__ float warp_norm2(const float2 (&v)[NR]) {
   return s;
 }
 
+// TB = thread bits of a tile: 8 -- the 8 compute warps share one tile stream;
+// 7 -- two groups of 4 warps, each with its own tile stream (tiles alternate
+// between the groups) and its own named barrier, so one group's shared-memory
+// transposes and conversions overlap the other's tensor-core work.
+template <int G>
+__device__ __forceinline__ void group_bar(int group) {
+  if constexpr (G == 1) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(kComputeThreads / G) : "memory");
+  }
+}
+
+// ------------------------------------- tcgen05 GEMM phase (two-stream tiles)
+// With 7 thread bits each warp group owns a 128-row tile; its 128 threads
+// hold one row each (32 complex amplitudes = the phase's register bits in
+// matrix order).  The phase D = A B runs on the 5th-generation tensor cores:
+// A (the rows, fp16 hi/lo split after per-row power-of-two scaling) is
+// written to TMEM with tcgen05.st, B (the real block form of the fused
+// 32x32 phase matrix, fp16 hi/lo, K-major core matrices) sits in shared
+// memory, ONE thread issues the 12 tcgen05.mma.kind::f16 (M 128, N 64, K 16;
+// terms h Bh + l Bh + h Bl) and commits to an mbarrier, and the rows come
+// back with tcgen05.ld.  Unlike warp-level mma.sync (which holds the
+// scheduler's issue slot ~8.5 cycles per HMMA on B200, tools/probes/
+// mma_overlap_probe.cu), the GEMM costs the issuing warps nothing, and the
+// other group's conversions and transposes overlap it.
+__device__ __forceinline__ void t5_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void t5_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void t5_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void t5_ld32(uint32_t taddr, uint32_t (&d)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+        "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]),
+        "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]),
+        "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+// shared-memory matrix descriptor: K-major, SWIZZLE_NONE, sm100 version bit
+__device__ __forceinline__ uint64_t t5_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor: D f32, A/B f16, both K-major, N = 64, M = 128
+constexpr uint32_t kT5Idesc = (1u << 4) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void t5_mma(uint32_t d, uint32_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n}" ::"r"(d),
+      "r"(a), "l"(b), "r"(acc), "r"(kT5Idesc)
+      : "memory");
+}
+
+// Bounded wait (a fault in the async pipeline must not hang the GPU).
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  for (long long i = 0; !mbar_try_wait_suspend(a, parity); ++i)
+    if (i > (1LL << 26)) __trap();
+}
+
+// One tcgen05 GEMM phase of a 128-row group.  tm = the group's TMEM base
+// (A hi at +0, A lo at +32, D at +64 columns); lane = this thread's row.
+// B: [hi 8 KB | lo 8 KB], offset(n, k) = (n/8) 1024 + (k/8) 128 + (n%8) 16 + (k%8) 2.
+template <int NTG>
+__device__ __forceinline__ void tc5_phase(float2 (&v)[32], uint32_t tm, int gt, uint32_t bmat, uint64_t* bar,
+                                          uint32_t& par, int group) {
+  const uint32_t tl = tm + (uint32_t(gt & ~31) << 16);  // this warp's lane quarter
+  float mx = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) mx = fmaxf(mx, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+  const int e = (__float_as_int(mx) >> 23) & 0xff;
+  const int se = min(max(268 - e, 1), 253);  // 2^(14 - exponent(mx)), clamped
+  const float sc = __int_as_float(se << 23), inv = __int_as_float((254 - se) << 23);
+  {
+    uint32_t hv[32], lv[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float xr = v[j].x * sc, xi = v[j].y * sc;
+      const uint32_t hh = pack_half2(xr, xi);
+      const float2 hf = unpack_half2(hh);
+      hv[j] = hh;
+      lv[j] = pack_half2(xr - hf.x, xi - hf.y);
+    }
+    t5_st32(tl + 0, hv);
+    t5_st32(tl + 32, lv);
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  t5_fence_before();
+  group_bar<kComputeThreads / NTG>(group);
+  if (gt == 0) {
+    t5_fence_after();
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint32_t a = tm + (t == 1 ? 32u : 0u) + 8u * ks;
+        const uint64_t b = t5_desc(bmat + (t == 2 ? 8192u : 0u) + 256u * ks, 128, 1024);
+        t5_mma(tm + 64, a, b, (t | ks) ? 1u : 0u);
+      }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+  }
+  mbar_wait_bounded(bar, par);
+  par ^= 1;
+  t5_fence_after();
+  uint32_t d[32];
+  t5_ld32(tl + 64, d);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = make_float2(__uint_as_float(d[2 * j]) * inv, __uint_as_float(d[2 * j + 1]) * inv);
+  t5_ld32(tl + 96, d);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    v[16 + j] = make_float2(__uint_as_float(d[2 * j]) * inv, __uint_as_float(d[2 * j + 1]) * inv);
+  t5_fence_before();
+}
+
 // Shared-memory layout of k_reg_pass: barriers | coefficient pool | thread
 // parts of the diagonal table indices | outside-tile parts (2S ring) | tiles.
 struct RegSmem {
@@ -293,7 +426,9 @@ __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(C), 128);
   l.dout = l.dthr + align_up(size_t(h.n_ops) * (size_t(1) << h.thread_bits), 128);
   l.red = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
-  l.mats = l.red + 256;  // [group][tile parity][start/end][warp] tile norms (renorm)
+  // [group][tile parity][start/end][warp] tile norms (renorm, 256 B), then the
+  // tcgen05 completion barriers [group] and the TMEM base address
+  l.mats = l.red + 384;
   l.tiles = l.mats + (h.mma_phases ? size_t(h.tc_count) * kMmaMatBytes : 0);
   l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
   return l;
@@ -362,19 +497,6 @@ struct GlobalAddr {
   }
 };
 
-// TB = thread bits of a tile: 8 -- the 8 compute warps share one tile stream;
-// 7 -- two groups of 4 warps, each with its own tile stream (tiles alternate
-// between the groups) and its own named barrier, so one group's shared-memory
-// transposes and conversions overlap the other's tensor-core work.
-template <int G>
-__device__ __forceinline__ void group_bar(int group) {
-  if constexpr (G == 1) {
-    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
-  } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(kComputeThreads / G) : "memory");
-  }
-}
-
 template <class C, int RB, int TB = 8>
 __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + TB;
@@ -393,15 +515,29 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
   const uint4* mats = reinterpret_cast<const uint4*>(smem + lay.mats);  // mma.sync B fragments
   float* red = reinterpret_cast<float*>(smem + lay.red);
+  uint64_t* t5bar = reinterpret_cast<uint64_t*>(smem + lay.red + 256);  // [group] tcgen05 commits
+  uint32_t* t5slot = reinterpret_cast<uint32_t*>(smem + lay.red + 256 + 16);
   C* tiles = reinterpret_cast<C*>(smem + lay.tiles);
   const int tid = threadIdx.x;
+  constexpr bool kT5 = sizeof(C) == 8 && RB == 5 && TB == 7;  // tcgen05 GEMM phases
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NTG);
     }
+    if constexpr (kT5) {
+      mbar_init(&t5bar[0], 1);
+      mbar_init(&t5bar[1], 1);
+    }
     fence_mbar_init();
+  }
+  if constexpr (kT5) {
+    if (h.mma_phases && tid < 32) {  // 2 groups x 128 TMEM columns
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_addr(t5slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
   if (h.mma_phases) {
@@ -413,7 +549,16 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
     const OpDesc& op = args.ops[e / NTG];
     dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
   }
+  if constexpr (kT5) {
+    fence_proxy_async_smem();  // B operands written by the generic proxy, read by the tensor core
+    t5_fence_before();
+  }
   __syncthreads();
+  uint32_t t5base = 0, t5par = 0;
+  if constexpr (kT5) {
+    t5_fence_after();
+    t5base = *t5slot;
+  }
   // outside-tile table bits of tile `it` (written by the producer before it
   // arms the stage's barrier; a 2S ring so a slot outlives its buffer).  The
   // whole producer warp computes it, one op per lane.
@@ -532,7 +677,13 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
           const float w = warp_norm2(v);
           if ((gt & 31) == 0) rp[gt >> 5] = w;
         }
-        if (ph.flags & PH_MMA) mma_phase(v, mats + size_t(ph.tc) * (kMmaMatBytes / 16), tid & 31);
+        if (ph.flags & PH_MMA) {
+          if constexpr (kT5)
+            tc5_phase<NTG>(v, t5base + uint32_t(group) * 128u, gt,
+                           smem_addr(mats) + uint32_t(ph.tc) * kMmaMatBytes, &t5bar[group], t5par, group);
+          else
+            mma_phase(v, mats + size_t(ph.tc) * (kMmaMatBytes / 16), tid & 31);
+        }
       }
       for (int o = ph.op_begin; o < ph.op_end; ++o) {
         const OpDesc& op = args.ops[o];
@@ -598,6 +749,15 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
     xs += NG;
     if (xs >= 2 * S) xs -= 2 * S;
     tpar ^= 1;
+  }
+  if constexpr (kT5) {
+    if (h.mma_phases) {  // every group done with TMEM before warp 0 frees it
+      asm volatile("bar.sync 3, %0;" ::"n"(kComputeThreads) : "memory");
+      if (tid < 32) {
+        t5_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(t5base) : "memory");
+      }
+    }
   }
 }
 

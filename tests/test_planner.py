@@ -179,12 +179,16 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                 R = ph["R"][:rb]
                 mp = ph["map"]
                 assert sorted(mp[:T]) == list(range(T)), mp  # the layout is a bit permutation
-                if ph["mma"]:
+                if ph["mma"] and T - rb == 8:
                     # fragment layout (svb_regpass.cuh mma_phase): K bits R[2..4] in
                     # registers 0..2, R[0..1] in lanes 0..1; the GEMM acts on R
                     assert mp[0:3] == R[2:5] and mp[5:7] == R[0:2], (mp, R)
                     assert ph["op_begin"] == ph["op_end"]
                     mp = list(R) + [q for q in range(T) if q not in R]
+                elif ph["mma"]:
+                    # tcgen05 phases (7 thread bits): one row per thread in matrix order
+                    assert mp[:T] == list(R) + [q for q in range(T) if q not in R], (mp, R)
+                    assert ph["op_begin"] == ph["op_end"]
                 base = np.zeros(nthreads, dtype=np.int64)
                 for k in range(T - rb):
                     base |= ((tid >> k) & 1) << mp[rb + k]
