@@ -56,6 +56,7 @@ def parse_args():
     ap.add_argument("--pass-times", action="store_true", help="print per-pass device times to stderr")
     ap.add_argument("--tensor-cores", type=int, default=0, help="1 on, -1 off, 0 default")
     ap.add_argument("--tc-min-dense", type=int, default=0)
+    ap.add_argument("--streams", type=int, default=0, help="tile streams per CTA (0 default)")
     return ap.parse_args()
 
 
@@ -272,7 +273,8 @@ def run_b200(args):
     opts = plan_options(cost_budget=args.cost_budget, stages=args.stages,
                         tile_bits=args.tile_bits, min_low_bits=args.min_low_bits,
                         reg_bits=args.reg_bits, no_reg_phases=int(args.no_reg_phases),
-                        tensor_cores=args.tensor_cores, tc_min_dense=args.tc_min_dense)
+                        tensor_cores=args.tensor_cores, tc_min_dense=args.tc_min_dense,
+                        streams=args.streams)
     eng = B200Engine("b200-bench", device=local, options=opts)
 
     if world > 1:

@@ -147,7 +147,8 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   // instantiated register kernels: c64 RB 3..5, c128 RB 3..4 (8 thread bits);
   // the tensor-core kernel: c64 RB 5 with 7 thread bits
   if (TB == 8 && (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4))) return false;
-  if (TB == 7 && (RB != 5 || prec != SVB_C64)) return false;  // k_tc_pass / k_reg_pass<float2, 5, 7>
+  // 7 thread bits: k_tc_pass / k_reg_pass<float2, 5, 7>, k_reg_pass<double2, 4, 7>
+  if (TB == 7 && !((RB == 5 && prec == SVB_C64) || (RB == 4 && prec == SVB_C128))) return false;
   if (p.T != RB + TB) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
@@ -751,7 +752,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   // c64 tensor-core phases: 12-qubit tiles in two warp-group streams with
   // tcgen05 GEMMs (measured layered-28 33.2 ms vs 43.3 ms for 13-qubit tiles
   // with mma.sync phases)
-  int T = opt.tile_bits > 0 ? opt.tile_bits : ((use_tc || use_mma) ? 12 : default_tile_bits(prec));
+  int T = opt.tile_bits > 0 ? opt.tile_bits
+          : ((use_tc || (use_mma && opt.streams != 1)) ? 12
+             : (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4)) ? 11
+                                                                                                : default_tile_bits(prec));
   // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)
   if (T > (prec == SVB_C64 ? 13 : 12)) T = prec == SVB_C64 ? 13 : 12;
   if (T > n) T = n;
@@ -988,9 +992,14 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     p.num_gates = int(taken.size());
     if (use_tc && p.T == 12 && build_phases(p, 5, prec, 7)) {
       fuse_tc_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxTcPerPass);
-    } else if (use_mma && p.T == 12 && build_phases(p, 5, prec, 7)) {
+    } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
       // 12-qubit tiles: two warp groups with their own tile streams (k_reg_pass TB 7)
       fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);
+    } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
+               build_phases(p, 4, prec, 7)) {
+      // c128 default: two tile streams of 11-qubit tiles, 16 amplitudes x 128
+      // threads each (measured layered-30 395 ms vs 422 ms for one stream of
+      // 12-qubit tiles: one group's transposes overlap the other's FP64 work)
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile
