@@ -50,7 +50,7 @@ typedef struct svb_plan svb_plan;
 /* Planner knobs; zero-initialise for defaults. */
 typedef struct svb_plan_options {
   int tile_bits;        /* qubits per shared-memory tile (0: 13 for c64, 12 for c128) */
-  int min_low_bits;     /* contiguous low qubits always in the tile (0: 512-B chunks) */
+  int min_low_bits;     /* contiguous low qubits always in the tile (0: 128-B chunks) */
   int max_ops_per_pass; /* 0: 48 (kernel limit)                                      */
   double cost_budget;   /* modelled compute per pass as a multiple of the pass's HBM
                            time; 0: default (7.0 c64, 5.0 c128), <0: unlimited       */

@@ -19,7 +19,11 @@ constexpr double kTcDefaultBudget = 3.0;
 // layered-30 450 ms vs 513 ms for 11-qubit tiles x 8 amplitudes at 2 CTAs/SM:
 // 4 register bits hold ~3 brickwork gates per phase instead of ~2)
 int default_tile_bits(int prec) { return prec == SVB_C64 ? 13 : 12; }
-int default_min_low_bits(int prec) { return prec == SVB_C64 ? 6 : 5; }
+// contiguous low qubits of every tile: 128-B chunks (c64 16 / c128 8
+// amplitudes) leave more strided tile qubits to the planner (measured:
+// layered-28 c64 19 -> 13 passes, 33.3 -> 29.0 ms; layered-30 c128 21 -> 15,
+// 395 -> 378 ms) at no loss of DRAM efficiency
+int default_min_low_bits(int prec) { return prec == SVB_C64 ? 4 : 3; }
 int default_reg_bits(int prec) { return prec == SVB_C64 ? 5 : 4; }
 double default_cost_budget(int prec) { return prec == SVB_C64 ? 7.0 : 5.0; }
 // tile = RB + 8 qubits for the register kernel

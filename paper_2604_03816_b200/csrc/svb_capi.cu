@@ -3,7 +3,7 @@
 // Thin host layer: argument validation, plan objects (planner.cpp) turned
 // into __grid_constant__ kernel parameter blocks, launch geometry (persistent
 // grid = SMs x resident CTAs), error mapping.  No device memory is owned by a
-// plan; reductions use stream-ordered scratch (cudaMallocAsync).
+// plan; reductions use a per-device scratch buffer allocated once.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
@@ -50,6 +50,13 @@ struct DeviceFacts {
   int ctas_per_sm_c64 = 0;
   int ctas_per_sm_c128 = 0;
   bool attrs_set = false;
+  // reduction scratch (device partials + pinned host copy), allocated once:
+  // stream-ordered cudaMallocAsync next to a 100+ GiB torch allocation was
+  // measured taking 10-1000 ms per call
+  double2* red_dev = nullptr;
+  double2* red_host = nullptr;
+  long long red_cap = 0;
+  std::mutex red_mu;
 };
 std::mutex g_dev_mu;
 DeviceFacts g_dev[64];
@@ -470,21 +477,25 @@ int dot_impl(const void* a, const void* b, long long n, double* out2, cudaStream
   const int threads = 512;
   long long grid = std::min<long long>((n + threads - 1) / threads, (long long)f->sm_count * 4);
   if (grid < 1) grid = 1;
-  double2* partial = nullptr;
-  SVB_CUDA(cudaMallocAsync(&partial, sizeof(double2) * grid, s));
-  k_dot<C><<<(unsigned)grid, threads, 0, s>>>(static_cast<const C*>(a), static_cast<const C*>(b), n, partial);
-  cudaError_t le = cudaGetLastError();
-  std::vector<double2> host(grid);
-  cudaError_t ce = le == cudaSuccess
-                       ? cudaMemcpyAsync(host.data(), partial, sizeof(double2) * grid, cudaMemcpyDeviceToHost, s)
-                       : le;
-  cudaFreeAsync(partial, s);
-  if (ce != cudaSuccess) return cuda_fail(ce, "svb_dot");
+  std::lock_guard<std::mutex> lk(f->red_mu);
+  if (f->red_cap < grid) {
+    if (f->red_dev) cudaFree(f->red_dev);
+    if (f->red_host) cudaFreeHost(f->red_host);
+    f->red_dev = nullptr;
+    f->red_host = nullptr;
+    f->red_cap = 0;
+    SVB_CUDA(cudaMalloc(&f->red_dev, sizeof(double2) * grid));
+    SVB_CUDA(cudaMallocHost(&f->red_host, sizeof(double2) * grid));
+    f->red_cap = grid;
+  }
+  k_dot<C><<<(unsigned)grid, threads, 0, s>>>(static_cast<const C*>(a), static_cast<const C*>(b), n, f->red_dev);
+  SVB_CUDA(cudaGetLastError());
+  SVB_CUDA(cudaMemcpyAsync(f->red_host, f->red_dev, sizeof(double2) * grid, cudaMemcpyDeviceToHost, s));
   SVB_CUDA(cudaStreamSynchronize(s));
   double re = 0.0, im = 0.0;
   for (long long i = 0; i < grid; ++i) {
-    re += host[i].x;
-    im += host[i].y;
+    re += f->red_host[i].x;
+    im += f->red_host[i].y;
   }
   out2[0] = re;
   out2[1] = im;

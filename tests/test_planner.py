@@ -117,7 +117,7 @@ def test_plan_structure_layered28():
         assert len(passes) < len(f.gates) / 2
         for p in passes:
             assert p["low_bits"] + len(p["high"]) == p["tile_bits"]
-            assert p["low_bits"] >= (6 if prec is Precision.SINGLE else 5)
+            assert p["low_bits"] >= (4 if prec is Precision.SINGLE else 3)
             assert p["reg_bits"] == (5 if prec is Precision.SINGLE else 4)
             assert p["tile_bits"] == 12 if prec is Precision.SINGLE else 11
 

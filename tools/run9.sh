@@ -1,9 +1,6 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 rm -f gpurun_out/sweep.txt
-for a in "--config qft30" "--config layered33" "--config layered-30 --precision double" "--config layered-30" "--config qft-28 --precision single"; do
+for a in "" "--config qft30" "--config layered33" "--config layered-30 --precision double" "--config layered-30" "--tensor-cores -1" "--config qft-28 --precision single"; do
   echo "ARGS $a :: $(timeout 400 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>&1 | tail -1)" >> gpurun_out/sweep.txt
 done
-timeout 600 python bench.py > gpurun_out/bench_default.txt 2>&1
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.txt 2>&1
-bash tools/ncu_full.sh 1 prof_c128_l30 --config layered-30 --precision double
