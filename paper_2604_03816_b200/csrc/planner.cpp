@@ -997,13 +997,17 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     if (use_tc && p.T == 12 && build_phases(p, 5, prec, 7)) {
       fuse_tc_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxTcPerPass);
     } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
-      // 12-qubit tiles: two warp groups with their own tile streams (k_reg_pass TB 7)
+      // 12-qubit tiles: warp groups with their own tile streams (k_reg_pass TB 7)
       fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);
+      // three streams by default (measured layered-28 26.4 ms vs 29.7 ms with
+      // two: more warp groups hide the per-phase TMEM / MMA / barrier latency)
+      p.streams = opt.streams == 2 ? 2 : 3;
     } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
                build_phases(p, 4, prec, 7)) {
       // c128 default: two tile streams of 11-qubit tiles, 16 amplitudes x 128
       // threads each (measured layered-30 395 ms vs 422 ms for one stream of
       // 12-qubit tiles: one group's transposes overlap the other's FP64 work)
+      p.streams = 2;
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile

@@ -82,6 +82,7 @@ struct Pass {
   bool tensor_cores = false;      // executed by k_tc_pass
   bool mma_phases = false;        // k_reg_pass with mma.sync GEMM phases (tc_mats)
   bool renorm = false;            // all ops unitary: the kernel restores each tile's norm
+  int streams = 1;                // tile streams per CTA (7 thread bits: 2 or 3)
   std::vector<std::vector<cd>> tc_mats;  // fused phase matrices (2^RB x 2^RB, row-major)
   std::vector<RegPhase> phases;
   std::vector<RegOp> reg_ops;     // same order as ops

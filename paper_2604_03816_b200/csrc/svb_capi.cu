@@ -78,6 +78,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
                          (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
+                         (const void*)k_reg_pass<float2, 5, 7, 3>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -133,6 +134,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.tc_count = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
   a.h.mma_phases = p.mma_phases ? 1 : 0;
   a.h.thread_bits = p.phases.empty() ? 8 : p.thread_bits;
+  a.h.streams = p.phases.empty() ? 1 : p.streams;
   a.h.renorm = p.renorm ? 1 : 0;
   a.h.tc_mats = nullptr;
   int off = 0;
@@ -284,7 +286,7 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     if constexpr (sizeof(C) == 8) {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 5) return fail(SVB_EUNSUPPORTED, "c64 reg_bits must be 3..5");
       if (a.h.thread_bits == 7 && a.h.reg_bits != 5) return fail(SVB_EUNSUPPORTED, "two-stream tiles need reg_bits 5");
-      fn = a.h.thread_bits == 7 ? k_reg_pass<C, 5, 7>
+      fn = a.h.thread_bits == 7 ? (a.h.streams == 3 ? k_reg_pass<C, 5, 7, 3> : k_reg_pass<C, 5, 7>)
            : a.h.reg_bits == 5  ? k_reg_pass<C, 5>
            : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
                                 : k_reg_pass<C, 3>;
@@ -299,18 +301,20 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
       if (a.ops[i].kind == OP_DENSE) kmax = std::max(kmax, a.ops[i].k);
     fn = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
   }
+  // k_reg_pass: 128 threads per tile stream (7 thread bits) or 256, + producer warp
+  const int block = a.h.n_phases > 0 && a.h.thread_bits == 7 && a.h.streams == 3 ? 3 * 128 + 32 : kThreads;
   if (a.h.stages == 0) {
     // Automatic TMA ring depth: the deepest ring that keeps the CTAs per SM of
     // a 2-stage ring (measured: resident warps matter more than ring depth --
     // qft-30 c128 141 ms at 2 stages / 2 CTAs vs 192 ms at 3 stages / 1 CTA).
     a.h.stages = 2;
     int occ2 = 0, occ = 0;
-    SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, kThreads, smem_of()));
+    SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, block, smem_of()));
     while (a.h.stages < 6) {
       ++a.h.stages;
       occ = 0;
       if (smem_of() <= size_t(f->max_smem))
-        SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem_of()));
+        SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem_of()));
       if (occ < occ2) {
         --a.h.stages;
         break;
@@ -320,15 +324,19 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   // deepest TMA ring that fits the opt-in shared memory (>= 2 stages); two
   // tile streams (7 thread bits) own alternate stages, so the ring is even
   while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
-  if (a.h.n_phases > 0 && a.h.thread_bits == 7 && (a.h.stages & 1)) --a.h.stages;
+  if (a.h.n_phases > 0 && a.h.thread_bits == 7) {  // stage s belongs to stream s % streams
+    const int g = a.h.streams == 3 ? 3 : 2;
+    a.h.stages = std::max(g, a.h.stages / g * g);
+    while (a.h.stages > g && smem_of() > size_t(f->max_smem)) a.h.stages -= g;
+  }
   const size_t smem = smem_of();
   int per_sm = 0;
-  SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+  SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tile pass does not fit on an SM (shared memory)");
   const long long n_tiles = a.h.n_tiles;
   long long grid = std::min<long long>(n_tiles, (long long)f->sm_count * per_sm);
   if (grid < 1) grid = 1;
-  fn<<<(unsigned)grid, kThreads, smem, stream>>>(amps, a);
+  fn<<<(unsigned)grid, block, smem, stream>>>(amps, a);
   SVB_CUDA(cudaGetLastError());
   (void)n_local;
   return SVB_OK;

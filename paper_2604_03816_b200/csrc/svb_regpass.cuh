@@ -285,12 +285,13 @@ __device__ __forceinline__ float warp_norm2(const float2 (&v)[NR]) {
 // 7 -- two groups of 4 warps, each with its own tile stream (tiles alternate
 // between the groups) and its own named barrier, so one group's shared-memory
 // transposes and conversions overlap the other's tensor-core work.
-template <int G>
+// Named barrier of one tile stream (ids 1..NG; NTHR threads each).
+template <int G, int NTHR>
 __device__ __forceinline__ void group_bar(int group) {
   if constexpr (G == 1) {
-    asm volatile("bar.sync 1, %0;" ::"n"(kComputeThreads) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory");
   } else {
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(kComputeThreads / G) : "memory");
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(NTHR) : "memory");
   }
 }
 
@@ -333,6 +334,20 @@ __device__ __forceinline__ void t5_ld32(uint32_t taddr, uint32_t (&d)[32]) {
       : "memory");
 }
 
+__device__ __forceinline__ void t5_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void t5_ld16(uint32_t taddr, uint32_t (&d)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+        "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 // shared-memory matrix descriptor: K-major, SWIZZLE_NONE, sm100 version bit
 __device__ __forceinline__ uint64_t t5_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
@@ -359,7 +374,7 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
 // One tcgen05 GEMM phase of a 128-row group.  tm = the group's TMEM base
 // (A hi at +0, A lo at +32, D at +64 columns); lane = this thread's row.
 // B: [hi 8 KB | lo 8 KB], offset(n, k) = (n/8) 1024 + (k/8) 128 + (n%8) 16 + (k%8) 2.
-template <int NTG>
+template <int NG, int NTG>
 __device__ __forceinline__ void tc5_phase(float2 (&v)[32], uint32_t tm, int gt, uint32_t bmat, uint64_t* bar,
                                           uint32_t& par, int group) {
   const uint32_t tl = tm + (uint32_t(gt & ~31) << 16);  // this warp's lane quarter
@@ -369,22 +384,25 @@ __device__ __forceinline__ void tc5_phase(float2 (&v)[32], uint32_t tm, int gt, 
   const int e = (__float_as_int(mx) >> 23) & 0xff;
   const int se = min(max(268 - e, 1), 253);  // 2^(14 - exponent(mx)), clamped
   const float sc = __int_as_float(se << 23), inv = __int_as_float((254 - se) << 23);
-  {
-    uint32_t hv[32], lv[32];
+  // convert and store in chunks of 8 columns (few live registers)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
+  for (int c = 0; c < 4; ++c) {
+    uint32_t hv[8], lv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = 8 * c + q;
       const float xr = v[j].x * sc, xi = v[j].y * sc;
       const uint32_t hh = pack_half2(xr, xi);
       const float2 hf = unpack_half2(hh);
-      hv[j] = hh;
-      lv[j] = pack_half2(xr - hf.x, xi - hf.y);
+      hv[q] = hh;
+      lv[q] = pack_half2(xr - hf.x, xi - hf.y);
     }
-    t5_st32(tl + 0, hv);
-    t5_st32(tl + 32, lv);
+    t5_st8(tl + 8 * c, hv);
+    t5_st8(tl + 32 + 8 * c, lv);
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   t5_fence_before();
-  group_bar<kComputeThreads / NTG>(group);
+  group_bar<NG, NTG>(group);
   if (gt == 0) {
     t5_fence_after();
 #pragma unroll
@@ -401,16 +419,15 @@ __device__ __forceinline__ void tc5_phase(float2 (&v)[32], uint32_t tm, int gt, 
   mbar_wait_bounded(bar, par);
   par ^= 1;
   t5_fence_after();
-  uint32_t d[32];
-  t5_ld32(tl + 64, d);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = make_float2(__uint_as_float(d[2 * j]) * inv, __uint_as_float(d[2 * j + 1]) * inv);
-  t5_ld32(tl + 96, d);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  for (int c = 0; c < 4; ++c) {
+    uint32_t d[16];
+    t5_ld16(tl + 64 + 16 * c, d);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    v[16 + j] = make_float2(__uint_as_float(d[2 * j]) * inv, __uint_as_float(d[2 * j + 1]) * inv);
+    for (int q = 0; q < 8; ++q)
+      v[8 * c + q] = make_float2(__uint_as_float(d[2 * q]) * inv, __uint_as_float(d[2 * q + 1]) * inv);
+  }
   t5_fence_before();
 }
 
@@ -428,7 +445,7 @@ __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
   l.red = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
   // [group][tile parity][start/end][warp] tile norms (renorm, 256 B), then the
   // tcgen05 completion barriers [group] and the TMEM base address
-  l.mats = l.red + 384;
+  l.mats = l.red + 512;  // renorm partials (<= 3 groups x 128 B), commit barriers, TMEM base
   l.tiles = l.mats + (h.mma_phases ? size_t(h.tc_count) * kMmaMatBytes : 0);
   l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
   return l;
@@ -497,13 +514,23 @@ struct GlobalAddr {
   }
 };
 
-template <class C, int RB, int TB = 8>
-__global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2) k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
+template <int TB, int NGRP>
+constexpr int reg_compute_threads() {
+  return (NGRP ? NGRP : kComputeThreads >> TB) << TB;
+}
+
+// NGRP: tile streams (0 = fill 256 compute threads); 3 streams of 128 threads
+// (c64 tcgen05 phases) make a 416-thread CTA.
+template <class C, int RB, int TB = 8, int NGRP = 0>
+__global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2)
+    k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + TB;
   constexpr int NR = 1 << RB;
-  constexpr int NTG = 1 << TB;                 // threads per tile stream
-  constexpr int NG = kComputeThreads / NTG;    // tile streams (warp groups)
-  constexpr int WPG = NTG / 32;                // warps per group
+  constexpr int NTG = 1 << TB;                          // threads per tile stream
+  constexpr int NCT = reg_compute_threads<TB, NGRP>();  // compute threads
+  constexpr int NG = NCT / NTG;                         // tile streams (warp groups)
+  constexpr int NTH = NCT + 32;                         // + the producer warp
+  constexpr int WPG = NTG / 32;                         // warps per group
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const int S = h.stages;
@@ -515,11 +542,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
   const uint4* mats = reinterpret_cast<const uint4*>(smem + lay.mats);  // mma.sync B fragments
   float* red = reinterpret_cast<float*>(smem + lay.red);
-  uint64_t* t5bar = reinterpret_cast<uint64_t*>(smem + lay.red + 256);  // [group] tcgen05 commits
-  uint32_t* t5slot = reinterpret_cast<uint32_t*>(smem + lay.red + 256 + 16);
+  uint64_t* t5bar = reinterpret_cast<uint64_t*>(smem + lay.red + 384);  // [group] tcgen05 commits
+  uint32_t* t5slot = reinterpret_cast<uint32_t*>(smem + lay.red + 384 + 32);
   C* tiles = reinterpret_cast<C*>(smem + lay.tiles);
   const int tid = threadIdx.x;
-  constexpr bool kT5 = sizeof(C) == 8 && RB == 5 && TB == 7;  // tcgen05 GEMM phases
+  constexpr bool kT5 = sizeof(C) == 8 && RB == 5 && TB == 7;  // tcgen05 GEMM phases (NG <= 3)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -527,25 +554,25 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
       mbar_init(&empty[s], NTG);
     }
     if constexpr (kT5) {
-      mbar_init(&t5bar[0], 1);
-      mbar_init(&t5bar[1], 1);
+      for (int g = 0; g < NG; ++g) mbar_init(&t5bar[g], 1);
     }
     fence_mbar_init();
   }
   if constexpr (kT5) {
-    if (h.mma_phases && tid < 32) {  // 2 groups x 128 TMEM columns
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_addr(t5slot))
+    if (h.mma_phases && tid < 32) {  // NG groups x 128 TMEM columns (power of two)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(t5slot)),
+                   "n"(NG > 2 ? 512 : 256)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
   }
-  for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  for (int e = tid; e < h.coeff_count; e += NTH) pool[e] = args.coeff[e];
   if (h.mma_phases) {
     const uint4* src = reinterpret_cast<const uint4*>(h.tc_mats);
     uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);
-    for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += kThreads) dst[e] = src[e];
+    for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += NTH) dst[e] = src[e];
   }
-  for (int e = tid; e < h.n_ops * NTG; e += kThreads) {
+  for (int e = tid; e < h.n_ops * NTG; e += NTH) {
     const OpDesc& op = args.ops[e / NTG];
     dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
   }
@@ -573,9 +600,9 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   const long long n_tiles = h.n_tiles;
   const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (tid >= kComputeThreads) {
+  if (tid >= NCT) {
     // ------------------------------------------------ producer: TMA loads only
-    const int lane = tid - kComputeThreads;
+    const int lane = tid - NCT;
     if (h.tma_rank > 0) {
       // one tensor-map load per (enumerated) sub-box: a single UTMALDG per tile
       // whenever the tile's qubit runs fit a rank-5 tensor map
@@ -654,20 +681,20 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
           // linear (TMA) layout -> swizzled layout through conflict-free reads
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[r * NTG + gt];
-          group_bar<NG>(group);
+          group_bar<NG, NTG>(group);
 #pragma unroll
           for (int r = 0; r < NR; ++r) buf[Swz<C>::f(r * NTG + gt)] = v[r];
-          group_bar<NG>(group);
+          group_bar<NG, NTG>(group);
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
         } else {
 #pragma unroll
           for (int r = 0; r < NR; ++r) v[r] = buf[a.lin(r)];
           // all reads of the linear layout finish before swizzled writes
-          if (np > 1 || tout) group_bar<NG>(group);
+          if (np > 1 || tout) group_bar<NG, NTG>(group);
         }
       } else {
-        group_bar<NG>(group);
+        group_bar<NG, NTG>(group);
 #pragma unroll
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
@@ -679,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         }
         if (ph.flags & PH_MMA) {
           if constexpr (kT5)
-            tc5_phase<NTG>(v, t5base + uint32_t(group) * 128u, gt,
+            tc5_phase<NG, NTG>(v, t5base + uint32_t(group) * 128u, gt,
                            smem_addr(mats) + uint32_t(ph.tc) * kMmaMatBytes, &t5bar[group], t5par, group);
           else
             mma_phase(v, mats + size_t(ph.tc) * (kMmaMatBytes / 16), tid & 31);
@@ -698,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
           // restore the tile's 2-norm (all ops of the pass are unitary)
           const float w = warp_norm2(v);
           if ((gt & 31) == 0) rp[8 + (gt >> 5)] = w;
-          group_bar<NG>(group);
+          group_bar<NG, NTG>(group);
           float n0 = 0.f, n1 = 0.f;
 #pragma unroll
           for (int i = 0; i < WPG; ++i) {
@@ -729,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
         // swizzled smem, then contiguous reads -> coalesced global stores
 #pragma unroll
         for (int r = 0; r < NR; ++r) buf[a.swz(r)] = v[r];
-        group_bar<NG>(group);
+        group_bar<NG, NTG>(group);
         // per-thread global offset of the linear layout x = rho * NTG + gt
         GlobalAddr<RB> lin_g;
         lin_g.gthr = global_of(gt, h);
@@ -752,10 +779,11 @@ __global__ void __launch_bounds__(kThreads, (sizeof(C) == 16 ? RB >= 4 : RB >= 5
   }
   if constexpr (kT5) {
     if (h.mma_phases) {  // every group done with TMEM before warp 0 frees it
-      asm volatile("bar.sync 3, %0;" ::"n"(kComputeThreads) : "memory");
+      asm volatile("bar.sync 7, %0;" ::"n"(NCT) : "memory");
       if (tid < 32) {
         t5_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(t5base) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(t5base), "n"(NG > 2 ? 512 : 256)
+                     : "memory");
       }
     }
   }

@@ -99,8 +99,8 @@ struct PassHeader {
   int mma_phases;               // k_reg_pass: tc_mats are mma.sync B fragments
   int renorm;                   // k_reg_pass (c64 RB 5): every op is unitary -- restore
                                 // each tile's 2-norm at the end of the pass
-  int thread_bits;              // k_reg_pass: 8 (one tile stream) or 7 (two warp groups)
-  int pad_tb;
+  int thread_bits;              // k_reg_pass: 8 (one tile stream) or 7 (warp groups of 128)
+  int streams;                  // k_reg_pass with 7 thread bits: 2 or 3 tile streams
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)
