@@ -1007,7 +1007,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       // c128 default: two tile streams of 11-qubit tiles, 16 amplitudes x 128
       // threads each (measured layered-30 395 ms vs 422 ms for one stream of
       // 12-qubit tiles: one group's transposes overlap the other's FP64 work)
-      p.streams = 2;
+      p.streams = opt.streams == 3 ? 3 : 2;
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile

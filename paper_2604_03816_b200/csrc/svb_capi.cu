@@ -78,7 +78,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
                          (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
-                         (const void*)k_reg_pass<float2, 5, 7, 3>,
+                         (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -293,7 +293,9 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     } else {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 4 || (a.h.thread_bits == 7 && a.h.reg_bits != 4))
         return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4 (two streams: 4)");
-      fn = a.h.thread_bits == 7 ? k_reg_pass<C, 4, 7> : a.h.reg_bits == 4 ? k_reg_pass<C, 4> : k_reg_pass<C, 3>;
+      fn = a.h.thread_bits == 7 ? (a.h.streams == 3 ? k_reg_pass<C, 4, 7, 3> : k_reg_pass<C, 4, 7>)
+           : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
+                                : k_reg_pass<C, 3>;
     }
   } else {
     int kmax = 0;
