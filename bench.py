@@ -261,9 +261,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SVB_DIST_BACKEND=gloo: exercise the N>1 path with several ranks sharing
+    # the devices of a smaller box (tests); NCCL over NVLink otherwise
+    backend_name = os.environ.get("SVB_DIST_BACKEND", "nccl")
+    if backend_name != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend_name == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend_name)
     cfg, kind, n, circuit, prec = workload(args, world)
     fused, rep = fuse(circuit, args.fuse_width)
     g0, gf = len(circuit.gates), len(fused.gates)
@@ -422,6 +430,7 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
 
     from paper_2604_03816_b200.sharded import CudaShardBackend, ShardedEngine, SwapStep
 
+    red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"  # gloo reduces host tensors
     backend = CudaShardBackend(local, eng.options)
     sh = ShardedEngine(backend)
     sched, progs = sh.compile(fused, precision)
@@ -460,16 +469,16 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
         stop.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-    t_ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device="cuda")
+    t_ms = torch.tensor([start.elapsed_time(stop)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_step = float(t_ms.item()) / args.steps
     local_ms = sum(a.elapsed_time(b) for e in evs for k_, a, b in e if k_ == "local") / args.steps
     swap_ms = sum(a.elapsed_time(b) for e in evs for k_, a, b in e if k_ == "swap") / args.steps
-    agg = torch.tensor([local_ms, swap_ms], dtype=torch.float64, device="cuda")
+    agg = torch.tensor([local_ms, swap_ms], dtype=torch.float64, device=red_dev)
     dist.all_reduce(agg, op=dist.ReduceOp.MAX)
     local_ms, swap_ms = (float(x) for x in agg.tolist())
     norm = backend.norm2(state)
-    nt = torch.tensor([norm], dtype=torch.float64, device="cuda")
+    nt = torch.tensor([norm], dtype=torch.float64, device=red_dev)
     dist.all_reduce(nt)
     bytes_per_pass = 2 * (1 << n_local) * amp_bytes
     peak, peak_kind = measured_peak_hbm()
@@ -485,7 +494,7 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
         t0 = time.perf_counter()
         st = sh.run_circuit(fused, precision)
         _ = st.norm_squared()
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         if k:
             e2e.append(float(dt.item()))
