@@ -1,13 +1,19 @@
 #!/bin/bash
-# One gpurun call: GPU tests, smoke, a bench line, and the ncu launch list.
-set -x
+# One gpurun call: GPU tests, smoke, the default bench line, every BASELINE
+# config, the reference arm, the ncu launch list and one full capture.
+#   /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash tools/gpu_check.sh'
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
-timeout 120 python __graft_entry__.py --smoke > gpurun_out/smoke0.txt 2>&1; echo "smoke0 rc=$?" >> gpurun_out/smoke0.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
-timeout 600 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.txt 2>&1; echo "bench rc=$?" >> gpurun_out/bench.txt
+timeout 600 python bench.py > gpurun_out/bench_default.txt 2>&1
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.txt 2>&1
+rm -f gpurun_out/sweep.txt
+for a in "--config qft30" "--config layered33" "--config layered-30 --precision double" "--config layered-30"; do
+  echo "ARGS $a :: $(timeout 400 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $a 2>&1 | tail -1)" >> gpurun_out/sweep.txt
+done
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -k regex:"k_(tile|reg|tc)_pass" -c 80 --csv --log-file gpurun_out/launches.csv \
+  -k regex:"k_(tile|reg|tc)_pass" -c 40 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-tail -3 gpurun_out/pytest_gpu.txt gpurun_out/smoke.txt gpurun_out/bench.txt
+bash tools/ncu_full.sh 3 prof_default
+tail -n 3 gpurun_out/pytest_gpu.txt gpurun_out/smoke.txt gpurun_out/bench_default.txt
