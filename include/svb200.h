@@ -67,7 +67,7 @@ typedef struct svb_plan_options {
   int no_window_search; /* 1: plain program-order greedy pass building             */
   int streams;          /* tile streams per CTA for register phases: 2 or 3 = warp
                            groups of 128 threads (7 thread bits), 1 = one stream of
-                           256; 0 = default (3: c64 tensor-core phases, 2: c128) */
+                           256; 0 = default (3, without a producer warp) */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */

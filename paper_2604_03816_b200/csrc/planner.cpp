@@ -1004,10 +1004,13 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       p.streams = opt.streams == 2 ? 2 : 3;
     } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
                build_phases(p, 4, prec, 7)) {
-      // c128 default: two tile streams of 11-qubit tiles, 16 amplitudes x 128
-      // threads each (measured layered-30 395 ms vs 422 ms for one stream of
-      // 12-qubit tiles: one group's transposes overlap the other's FP64 work)
-      p.streams = opt.streams == 3 ? 3 : 2;
+      // c128 default: tile streams of 11-qubit tiles, 16 amplitudes x 128
+      // threads each (measured layered-30 395 ms with two vs 422 ms for one
+      // stream of 12-qubit tiles: one group's transposes overlap another's
+      // FP64 work)
+      // three producer-free streams by default (measured layered-30 332 ms vs
+      // 379 ms with two, qft-30 121 vs 131 ms)
+      p.streams = opt.streams == 2 ? 2 : 3;
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile

@@ -304,7 +304,8 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     fn = kmax <= 2 ? k_tile_pass<C, 2> : kmax <= 3 ? k_tile_pass<C, 3> : k_tile_pass<C, 6>;
   }
   // k_reg_pass: 128 threads per tile stream (7 thread bits) or 256, + producer warp
-  const int block = a.h.n_phases > 0 && a.h.thread_bits == 7 && a.h.streams == 3 ? 3 * 128 + 32 : kThreads;
+  // (three streams have no producer warp: each loads its own tiles)
+  const int block = a.h.n_phases > 0 && a.h.thread_bits == 7 && a.h.streams == 3 ? 3 * 128 : kThreads;
   if (a.h.stages == 0) {
     // Automatic TMA ring depth: the deepest ring that keeps the CTAs per SM of
     // a 2-stage ring (measured: resident warps matter more than ring depth --
@@ -328,7 +329,7 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
   if (a.h.n_phases > 0 && a.h.thread_bits == 7) {  // stage s belongs to stream s % streams
     const int g = a.h.streams == 3 ? 3 : 2;
-    a.h.stages = std::max(g, a.h.stages / g * g);
+    a.h.stages = a.h.streams == 3 ? 3 : std::max(g, a.h.stages / g * g);  // 3 streams: one stage each
     while (a.h.stages > g && smem_of() > size_t(f->max_smem)) a.h.stages -= g;
   }
   const size_t smem = smem_of();

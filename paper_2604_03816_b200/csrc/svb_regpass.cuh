@@ -518,18 +518,30 @@ template <int TB, int NGRP>
 constexpr int reg_compute_threads() {
   return (NGRP ? NGRP : kComputeThreads >> TB) << TB;
 }
+// Three tile streams run without a producer warp (each stream loads its own
+// tiles, one stage each): 12 warps keep 3 per scheduler, which allows 168
+// registers per thread instead of the 128 a 13th warp would impose.
+template <int TB, int NGRP>
+constexpr bool reg_no_producer() {
+  return NGRP == 3;
+}
+template <int TB, int NGRP>
+constexpr int reg_block_threads() {
+  return reg_compute_threads<TB, NGRP>() + (reg_no_producer<TB, NGRP>() ? 0 : 32);
+}
 
 // NGRP: tile streams (0 = fill 256 compute threads); 3 streams of 128 threads
 // (c64 tcgen05 phases) make a 416-thread CTA.
 template <class C, int RB, int TB = 8, int NGRP = 0>
-__global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2)
+__global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2)
     k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + TB;
   constexpr int NR = 1 << RB;
   constexpr int NTG = 1 << TB;                          // threads per tile stream
   constexpr int NCT = reg_compute_threads<TB, NGRP>();  // compute threads
   constexpr int NG = NCT / NTG;                         // tile streams (warp groups)
-  constexpr int NTH = NCT + 32;                         // + the producer warp
+  constexpr bool kNP = reg_no_producer<TB, NGRP>();     // streams load their own tiles
+  constexpr int NTH = reg_block_threads<TB, NGRP>();    // (+ the producer warp)
   constexpr int WPG = NTG / 32;                         // warps per group
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
@@ -600,7 +612,46 @@ __global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(
   const long long n_tiles = h.n_tiles;
   const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  if (tid >= NCT) {
+  // one stream's tile load (kNP: issued by warp 0 of the stream; lane 0 arms the
+  // barrier and issues the TMA, all lanes publish the outside-tile parts)
+  auto stream_load = [&](long long it, int st, int lane) {
+    const long long tile = (long long)blockIdx.x + it * gridDim.x;
+    if (h.has_outside) publish_outside(int(it % (2 * S)), tile, lane);
+    C* buf = tiles + (size_t(st) << T);
+    const long long tb = tile_base(tile, h);
+    if (h.tma_rank > 0) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[st], uint32_t(sizeof(C)) << T);
+        const int ne = h.n_enum;
+        const int sub = T - ne;
+        for (int e = 0; e < (1 << ne); ++e) {
+          long long origin = tb;
+          for (int j = 0; j < ne; ++j)
+            if ((e >> j) & 1) origin += 1LL << h.high[h.m - ne + j];
+          const long long w = origin << h.word_shift;
+          int c[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d)
+            c[d] = (d < h.tma_rank && h.tma_box[d] == 0) ? int((w >> h.tma_start[d]) & ((1LL << h.tma_bits[d]) - 1)) : 0;
+          tma_load(buf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[st]);
+        }
+      }
+    } else {
+      const int n_chunks = 1 << h.m;
+      const uint32_t chunk_bytes = uint32_t(sizeof(C)) << h.L;
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], chunk_bytes * uint32_t(n_chunks));
+      __syncwarp();
+      const uint64_t pol = policy_evict_first();
+      for (int c = lane; c < n_chunks; c += 32)
+        bulk_load(buf + (size_t(c) << h.L), amps + tb + chunk_offset(c, h), chunk_bytes, &full[st], pol);
+    }
+    __syncwarp();
+  };
+  if constexpr (kNP) {
+    (void)stream_load;
+  }
+
+  if (!kNP && tid >= NCT) {
     // ------------------------------------------------ producer: TMA loads only
     const int lane = tid - NCT;
     if (h.tma_rank > 0) {
@@ -661,9 +712,12 @@ __global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(
   // from the pass description: keeping 2 x RB 64-bit offsets live across the
   // tile loop would cost ~24 registers the tensor-core phases need
   // stage / barrier parity / outside-index slot / renorm slot of tile `it`,
-  // advanced incrementally (S is even when NG == 2)
+  // advanced incrementally (S is a multiple of NG)
   int s = group, xs = group, tpar = 0;
   uint32_t parity = 0;
+  if constexpr (kNP) {  // each stream owns stage `group`: load its first tile
+    if ((gt >> 5) == 0 && group < mine) stream_load(group, group, gt & 31);
+  }
   for (long long it = group; it < mine; it += NG) {
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
@@ -698,7 +752,17 @@ __global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(
 #pragma unroll
         for (int r = 0; r < NR; ++r) v[r] = buf[a.swz(r)];
       }
-      if (last && !tout) mbar_arrive(&empty[s]);  // buffer free for the next load
+      if (last && !tout) {
+        mbar_arrive(&empty[s]);  // buffer free for the next load
+        if constexpr (kNP) {
+          // warp 0 of the stream refills the stage with the stream's next tile
+          // as soon as every thread has read it (overlaps this last phase)
+          if ((gt >> 5) == 0 && it + NG < mine) {
+            mbar_wait(&empty[s], parity);
+            stream_load(it + NG, s, gt & 31);
+          }
+        }
+      }
       if constexpr (sizeof(C) == 8 && RB == 5) {
         if (p == 0 && h.renorm) {
           const float w = warp_norm2(v);
@@ -766,6 +830,12 @@ __global__ void __launch_bounds__(reg_compute_threads<TB, NGRP>() + 32, (sizeof(
 #pragma unroll
         for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * NTG + gt)];
         mbar_arrive(&empty[s]);
+        if constexpr (kNP) {
+          if ((gt >> 5) == 0 && it + NG < mine) {
+            mbar_wait(&empty[s], parity);
+            stream_load(it + NG, s, gt & 31);
+          }
+        }
       }
     }
     s += NG;
