@@ -345,6 +345,27 @@ def run_b200(args):
     peak, peak_kind = measured_peak_hbm()
     best_pass = min(pass_ms)
 
+    # single-gate pass (the north star's "per local gate pass"): one dense 2q
+    # gate = one HBM round trip of the state with no compute to hide, timed
+    # with CUDA events over 10 launches
+    from paper_2604_03816_b200.circuit import Circuit as _Circ
+    from paper_2604_03816_b200.circuit import GateKind as _GK
+    from paper_2604_03816_b200.circuit import GateOp as _GO
+    _rng = np.random.default_rng(5)
+    _u, _ = np.linalg.qr(_rng.normal(size=(4, 4)) + 1j * _rng.normal(size=(4, 4)))
+    gplan = eng.plan(_Circ(n, [_GO(_GK.CUSTOM, (3, n - 2), (), _u)]), precision)
+    gplan.execute(state.tensor, s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(10):
+        gplan.execute(state.tensor, s)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    gate_ms = e0.elapsed_time(e1) / 10
+    gate_pass = {"what": f"one dense 2q gate on qubits (3, {n - 2}) = one pass, 10 launches",
+                 "ms": gate_ms, "achieved": bytes_per_pass / (gate_ms / 1e3) / 1e9,
+                 "frac": bytes_per_pass / (gate_ms / 1e3) / 1e9 / peak}
+
     # e2e: public API from a host circuit: plan + launch (kernel-parameter H2D) +
     # run + device->host read of the result (norm^2 and amplitude 0)
     eng.release(state)
@@ -406,6 +427,7 @@ def run_b200(args):
                      "kernel": plan_kernels(plan), "bytes_per_launch": bytes_per_pass,
                      "avg_launch_ms": avg_pass_ms, "best_launch_ms": best_pass,
                      "best_frac": bytes_per_pass / (best_pass / 1e3) / 1e9 / peak,
+                     "single_gate_pass": gate_pass,
                      "compute": {"bound": "fp32-fma" if prec == "single" else "fp64-fma",
                                  "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                                  "frac": achieved_tflops / peak_tflops,
