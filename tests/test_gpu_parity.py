@@ -142,6 +142,47 @@ def test_qft18_outside_tile_diagonals(eng, prec):
     assert_close(eng.run_circuit(raw, Precision(prec)).amplitudes, orc.run_circuit(raw, prec), prec, "qft16 raw")
 
 
+@pytest.mark.parametrize("prec", ["double", "single"])
+def test_non_unitary_and_unnormalised(eng, prec):
+    """CUSTOM matrices need not be unitary and adopted states need not be
+    normalised (the reference applies whatever it is given): the tensor-core
+    phases' per-row scaling adapts to any magnitude and passes with a
+    non-unitary op skip the norm restoration."""
+    rng = np.random.default_rng(21)
+    n = 15
+    gates = []
+    for layer in range(6):
+        for q in range(layer % 2, n - 1, 2):
+            m = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+            if (layer + q) % 3:
+                m, _ = np.linalg.qr(m)
+            else:
+                m = 0.7 * m  # non-unitary
+            gates.append(GateOp(GateKind.CUSTOM, (q, q + 1), (), m))
+    c = Circuit(n, gates)
+    init = (rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)) * 3.0
+    init = init.astype(np.complex128 if prec == "double" else np.complex64)
+    st = eng.adopt(n, Precision(prec), init.copy())
+    for op in c.gates:  # per-gate path
+        eng.apply_gate(st, op)
+    want = init.copy()
+    for op in c.gates:
+        orc.apply_gate(want, n, op)
+    got = st.amplitudes
+    scale = float(np.abs(want).max())
+    err = float(np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max()) / scale
+    assert err <= (1e-12 if prec == "double" else 1e-5), err
+    eng.release(st)
+    # the planned path (fused phases, tensor cores for c64) from the same state
+    plan = eng.plan(c, Precision(prec))
+    st = eng.adopt(n, Precision(prec), init.copy())
+    eng.execute(st, plan)
+    got = st.amplitudes
+    err = float(np.abs(got.astype(np.complex128) - want.astype(np.complex128)).max()) / scale
+    assert err <= (1e-12 if prec == "double" else 1e-5), err
+    eng.release(st)
+
+
 def test_layered20_config1_vs_oracle(eng):
     """BASELINE config 1 workload (layered-20, c128, fused 693 -> 133)."""
     f, rep = fuse(gen.layered_circuit(20), 2)
