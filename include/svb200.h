@@ -65,9 +65,10 @@ typedef struct svb_plan_options {
                            experimental); 0 = default (2 for c64), -1 = off */
   int tc_min_dense;     /* dense gates a phase needs to become a GEMM (0: 2)         */
   int no_window_search; /* 1: plain program-order greedy pass building             */
-  int streams;          /* tile streams per CTA for register phases: 2 or 3 = warp
-                           groups of 128 threads (7 thread bits), 1 = one stream of
-                           256; 0 = default (3, without a producer warp) */
+  int streams;          /* tile streams per CTA for register phases: 2..4 = warp
+                           groups of 128 threads (7 thread bits; 3-4 without a
+                           producer warp), 1 = one stream of 256; 0 = default
+                           (4 for c64 tensor-core phases, 3 for c128)           */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */

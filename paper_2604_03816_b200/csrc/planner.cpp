@@ -1004,9 +1004,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
       // 12-qubit tiles: warp groups with their own tile streams (k_reg_pass TB 7)
       fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);
-      // three streams by default (measured layered-28 26.4 ms vs 29.7 ms with
-      // two: more warp groups hide the per-phase TMEM / MMA / barrier latency)
-      p.streams = opt.streams == 2 ? 2 : 3;
+      // four streams by default (measured layered-28 25.0 ms vs 25.8 with
+      // three and 29.7 with two: more warp groups hide the per-phase TMEM /
+      // MMA / barrier latency; 16 warps keep 128 registers per thread)
+      p.streams = opt.streams == 2 ? 2 : opt.streams == 3 ? 3 : 4;
     } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
                build_phases(p, 4, prec, 7)) {
       // c128 default: tile streams of 11-qubit tiles, 16 amplitudes x 128

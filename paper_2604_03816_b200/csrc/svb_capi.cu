@@ -79,6 +79,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
+                         (const void*)k_reg_pass<float2, 5, 7, 4>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
@@ -286,7 +287,8 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     if constexpr (sizeof(C) == 8) {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 5) return fail(SVB_EUNSUPPORTED, "c64 reg_bits must be 3..5");
       if (a.h.thread_bits == 7 && a.h.reg_bits != 5) return fail(SVB_EUNSUPPORTED, "two-stream tiles need reg_bits 5");
-      fn = a.h.thread_bits == 7 ? (a.h.streams == 3 ? k_reg_pass<C, 5, 7, 3> : k_reg_pass<C, 5, 7>)
+      fn = a.h.thread_bits == 7 ? (a.h.streams == 4 ? k_reg_pass<C, 5, 7, 4>
+                                   : a.h.streams == 3 ? k_reg_pass<C, 5, 7, 3> : k_reg_pass<C, 5, 7>)
            : a.h.reg_bits == 5  ? k_reg_pass<C, 5>
            : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
                                 : k_reg_pass<C, 3>;
@@ -305,7 +307,7 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   }
   // k_reg_pass: 128 threads per tile stream (7 thread bits) or 256, + producer warp
   // (three streams have no producer warp: each loads its own tiles)
-  const int block = a.h.n_phases > 0 && a.h.thread_bits == 7 && a.h.streams == 3 ? 3 * 128 : kThreads;
+  const int block = a.h.n_phases > 0 && a.h.thread_bits == 7 && a.h.streams >= 3 ? a.h.streams * 128 : kThreads;
   if (a.h.stages == 0) {
     // Automatic TMA ring depth: the deepest ring that keeps the CTAs per SM of
     // a 2-stage ring (measured: resident warps matter more than ring depth --
@@ -328,8 +330,8 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   // tile streams (7 thread bits) own alternate stages, so the ring is even
   while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
   if (a.h.n_phases > 0 && a.h.thread_bits == 7) {  // stage s belongs to stream s % streams
-    const int g = a.h.streams == 3 ? 3 : 2;
-    a.h.stages = a.h.streams == 3 ? 3 : std::max(g, a.h.stages / g * g);  // 3 streams: one stage each
+    const int g = a.h.streams >= 3 ? a.h.streams : 2;
+    a.h.stages = a.h.streams >= 3 ? a.h.streams : std::max(g, a.h.stages / g * g);  // 3-4 streams: one stage each
     while (a.h.stages > g && smem_of() > size_t(f->max_smem)) a.h.stages -= g;
   }
   const size_t smem = smem_of();

@@ -445,7 +445,7 @@ __host__ __device__ inline RegSmem reg_smem_layout(const PassHeader& h) {
   l.red = l.dout + align_up(size_t(2 * h.stages) * kMaxOps * sizeof(int), 128);
   // [group][tile parity][start/end][warp] tile norms (renorm, 256 B), then the
   // tcgen05 completion barriers [group] and the TMEM base address
-  l.mats = l.red + 512;  // renorm partials (<= 3 groups x 128 B), commit barriers, TMEM base
+  l.mats = l.red + 640;  // renorm partials (<= 4 groups x 128 B), commit barriers, TMEM base
   l.tiles = l.mats + (h.mma_phases ? size_t(h.tc_count) * kMmaMatBytes : 0);
   l.total = l.tiles + size_t(h.stages) * (sizeof(C) << h.T);
   return l;
@@ -523,7 +523,7 @@ constexpr int reg_compute_threads() {
 // registers per thread instead of the 128 a 13th warp would impose.
 template <int TB, int NGRP>
 constexpr bool reg_no_producer() {
-  return NGRP == 3;
+  return NGRP >= 3;
 }
 template <int TB, int NGRP>
 constexpr int reg_block_threads() {
@@ -554,8 +554,8 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [2S][op]: outside-tile part, per tile
   const uint4* mats = reinterpret_cast<const uint4*>(smem + lay.mats);  // mma.sync B fragments
   float* red = reinterpret_cast<float*>(smem + lay.red);
-  uint64_t* t5bar = reinterpret_cast<uint64_t*>(smem + lay.red + 384);  // [group] tcgen05 commits
-  uint32_t* t5slot = reinterpret_cast<uint32_t*>(smem + lay.red + 384 + 32);
+  uint64_t* t5bar = reinterpret_cast<uint64_t*>(smem + lay.red + 512);  // [group] tcgen05 commits
+  uint32_t* t5slot = reinterpret_cast<uint32_t*>(smem + lay.red + 512 + 32);
   C* tiles = reinterpret_cast<C*>(smem + lay.tiles);
   const int tid = threadIdx.x;
   constexpr bool kT5 = sizeof(C) == 8 && RB == 5 && TB == 7;  // tcgen05 GEMM phases (NG <= 3)
