@@ -1007,7 +1007,10 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       // four streams by default (measured layered-28 25.0 ms vs 25.8 with
       // three and 29.7 with two: more warp groups hide the per-phase TMEM /
       // MMA / barrier latency; 16 warps keep 128 registers per thread)
-      p.streams = opt.streams == 2 ? 2 : opt.streams == 3 ? 3 : 4;
+      // (a pass without tensor-core phases is HBM-bound: three streams keep
+      // more of each SM's shared memory for loads in flight -- single-gate
+      // pass 93 % of HBM vs 80 % with four)
+      p.streams = opt.streams == 2 ? 2 : opt.streams == 3 ? 3 : opt.streams == 4 ? 4 : (p.mma_phases ? 4 : 3);
     } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
                build_phases(p, 4, prec, 7)) {
       // c128 default: tile streams of 11-qubit tiles, 16 amplitudes x 128
