@@ -510,9 +510,15 @@ void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
       if (ro.kind == OP_DENSE) ++dense;
       else ok = ro.mask == 0 && ro.kx == 0;  // diagonal on register bits only
     }
-    if (ok && dense >= min_dense) cands.push_back({dense, f});
+    if (ok && dense >= 1) cands.push_back({dense, f});
   }
-  if (cands.empty()) return;
+  // a pass goes to the tensor cores when one of its phases holds min_dense
+  // dense ops; then every register-only phase does (measured: single-op
+  // phases in a tensor-core pass are cheaper as GEMMs, layered-28 25.0 ->
+  // 24.3 ms; an HBM-bound pass of single ops stays on the FMA pipes)
+  bool any = false;
+  for (const Cand& c : cands) any = any || c.dense >= min_dense;
+  if (!any) return;
   std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {
     return x.dense != y.dense ? x.dense > y.dense : x.phase < y.phase;
   });
