@@ -71,7 +71,7 @@ constexpr int kMaxTcPerPassDev = 2;
 // n = 2j + re/im of the output), split B = Bh + Bl in fp16 and stored in
 // m16n8k16 B-fragment order: [nt 0..7][kk 0..3][lane 0..31] x {bh0, bh1, bl0, bl1}.
 constexpr int kMmaMatBytes = 8 * 4 * 32 * 16;
-constexpr int kMaxMmaPerPass = 4;
+constexpr int kMaxMmaPerPass = 5;  // 5 x 16 KB + 4 tile streams x 32 KB fit 227 KB
 
 struct PassHeader {
   int T, L, m, n_ops;
