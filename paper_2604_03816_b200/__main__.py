@@ -1,6 +1,6 @@
-"""``python -m paper_2604_03816_b200`` -- the reference CLI's ``run`` and
-``bench-scaling`` subcommands (ref ``pkg/src/aqsim/cli.py:194-337``) for the
-B200 engine.
+"""``python -m paper_2604_03816_b200`` -- the reference CLI's ``run``,
+``bench-scaling`` and ``bench-fusion`` subcommands (ref
+``pkg/src/aqsim/cli.py:194-381``) for the B200 engine.
 
 Differences from ``aqsim run``: no memory governor / CPU fallback (the north
 star removes it; the device refuses with ``AllocationError`` instead), and
@@ -109,6 +109,36 @@ def cmd_bench_scaling(args) -> int:
     return 0
 
 
+def cmd_bench_fusion(args) -> int:
+    """Depth reduction and time of each circuit unfused vs fused (ref
+    cli.py:340-381; JSON rows instead of the reference's table)."""
+    eng = B200Engine("b200-cli")
+    rows = []
+    for spec in (s_.strip() for s_ in args.circuits.split(",") if s_.strip()):
+        circuit = _load(spec, args.seed)
+        fused, rep = fuse(circuit, args.fuse_width)
+
+        def _median_run(target) -> float:
+            times = []
+            for _ in range(args.repetitions):
+                t0 = time.perf_counter()
+                s = eng.run_circuit(target, Precision.DOUBLE)
+                times.append(time.perf_counter() - t0)
+                eng.release(s)
+            return statistics.median(times)
+
+        if args.no_exec or args.no_timing:
+            time_s = fused_time_s = 0.0
+        else:
+            time_s = _median_run(circuit)
+            fused_time_s = _median_run(fused)
+        rows.append({"circuit": getattr(circuit, "name", "") or spec, "original_depth": rep.original_depth,
+                     "fused_depth": rep.fused_depth, "reduction_percent": round(rep.reduction_percent, 1),
+                     "time_s": time_s, "fused_time_s": fused_time_s})
+    sys.stdout.write(json.dumps(rows, indent=2, sort_keys=True) + "\n")
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2604_03816_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -128,9 +158,16 @@ def main(argv=None) -> int:
     b.add_argument("--repetitions", type=int, default=3)
     b.add_argument("--seed", type=int, default=0)
     b.add_argument("--no-timing", action="store_true")
+    f = sub.add_parser("bench-fusion")
+    f.add_argument("--circuits", default="qft-12,ghz-12,random-12")
+    f.add_argument("--fuse-width", type=int, default=2)
+    f.add_argument("--repetitions", type=int, default=3)
+    f.add_argument("--seed", type=int, default=0)
+    f.add_argument("--no-exec", action="store_true")
+    f.add_argument("--no-timing", action="store_true")
     args = ap.parse_args(argv)
     try:
-        return cmd_run(args) if args.cmd == "run" else cmd_bench_scaling(args)
+        return {"run": cmd_run, "bench-scaling": cmd_bench_scaling, "bench-fusion": cmd_bench_fusion}[args.cmd](args)
     except ValueError as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 2

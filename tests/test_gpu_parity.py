@@ -327,6 +327,9 @@ def test_cli_run_and_bench_scaling(capsys):
     assert main(["bench-scaling", "--qubits", "10,12", "--repetitions", "1", "--no-timing"]) == 0
     rows = _json.loads(capsys.readouterr().out)
     assert [r["n"] for r in rows] == [10, 12]
+    assert main(["bench-fusion", "--circuits", "qft-10", "--repetitions", "1"]) == 0
+    rows = _json.loads(capsys.readouterr().out)
+    assert rows[0]["fused_time_s"] > 0
 
 
 def _sharded_cuda_worker(rank, world, port, out):
