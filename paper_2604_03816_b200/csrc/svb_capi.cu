@@ -335,6 +335,7 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     while (a.h.stages > g && smem_of() > size_t(f->max_smem)) a.h.stages -= g;
   }
   const size_t smem = smem_of();
+  if (a.h.n_tiles >= (1LL << 31)) return fail(SVB_EUNSUPPORTED, "more than 2^31 tiles per shard");
   int per_sm = 0;
   SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
   if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tile pass does not fit on an SM (shared memory)");

@@ -609,13 +609,15 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
     __syncwarp();
   };
 
-  const long long n_tiles = h.n_tiles;
-  const long long mine = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // tile counts fit 32 bits (a shard of <= 2^34 amplitudes in >= 2^11-amplitude
+  // tiles; the host checks): 32-bit loop state keeps registers free
+  const int n_tiles = int(h.n_tiles);
+  const int mine = int(blockIdx.x) < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
 
   // one stream's tile load (kNP: issued by warp 0 of the stream; lane 0 arms the
   // barrier and issues the TMA, all lanes publish the outside-tile parts)
-  auto stream_load = [&](long long it, int st, int lane) {
-    const long long tile = (long long)blockIdx.x + it * gridDim.x;
+  auto stream_load = [&](int it, int st, int lane) {
+    const int tile = int(blockIdx.x) + it * int(gridDim.x);
     if (h.has_outside) publish_outside(int(it % (2 * S)), tile, lane);
     C* buf = tiles + (size_t(st) << T);
     const long long tb = tile_base(tile, h);
@@ -718,8 +720,8 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
   if constexpr (kNP) {  // each stream owns stage `group`: load its first tile
     if ((gt >> 5) == 0 && group < mine) stream_load(group, group, gt & 31);
   }
-  for (long long it = group; it < mine; it += NG) {
-    const long long tile = (long long)blockIdx.x + it * gridDim.x;
+  for (int it = group; it < mine; it += NG) {
+    const int tile = int(blockIdx.x) + it * int(gridDim.x);
     C* buf = tiles + (size_t(s) << T);
     const long long origin = tile_base(tile, h);
     float* rp = red + (group * 2 + tpar) * 16;  // renorm partials of this tile
