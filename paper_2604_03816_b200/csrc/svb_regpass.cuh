@@ -364,11 +364,19 @@ __device__ __forceinline__ void t5_mma(uint32_t d, uint32_t a, uint64_t b, uint3
       : "memory");
 }
 
-// Bounded wait (a fault in the async pipeline must not hang the GPU).
+// Bounded wait (a fault in the async pipeline must not hang the GPU): traps
+// after 4 s of wall time (%globaltimer), far above any legitimate wait.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_addr(bar);
-  for (long long i = 0; !mbar_try_wait_suspend(a, parity); ++i)
-    if (i > (1LL << 26)) __trap();
+  if (mbar_try_wait_suspend(a, parity)) return;
+  const unsigned long long t0 = global_ns();
+  while (!mbar_try_wait_suspend(a, parity))
+    if (global_ns() - t0 > 4000000000ULL) __trap();
 }
 
 // One tcgen05 GEMM phase of a 128-row group.  tm = the group's TMEM base

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
       int s = 0;
       uint32_t ph = 0;
       for (long long it = 0; it < mine; ++it) {
-        if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
+        if (it >= S) mbar_wait_bounded(&empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&full[s], uint32_t(sizeof(C)) << T);
         const long long tb = tile_base((long long)blockIdx.x + it * gridDim.x, h);
         C* buf = tiles + (size_t(s) << T);
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
     const uint64_t pol = policy_evict_first();
     for (long long it = 0; it < mine; ++it) {
       const int s = int(it % S);
-      if (it >= S) mbar_wait_sleep(&empty[s], uint32_t(((it - S) / S) & 1));
+      if (it >= S) mbar_wait_bounded(&empty[s], uint32_t(((it - S) / S) & 1));
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&full[s], chunk_bytes * uint32_t(n_chunks));
       __syncwarp();
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
     const long long tile = (long long)blockIdx.x + it * gridDim.x;
     C* buf = tiles + (size_t(s) << T);
     const long long origin = tile_base(tile, h);
-    mbar_wait(&full[s], parity);
+    mbar_wait_bounded(&full[s], parity);
     C v[NR];
     for (int p = 0; p < np; ++p) {
       const PhaseDesc& ph = args.phases[p];
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_pass(float2* __restrict__ 
                            smem_addr(mma_bar))
                        : "memory");
         }
-        mbar_wait(mma_bar, mma_parity);
+        mbar_wait_bounded(mma_bar, mma_parity);
         mma_parity ^= 1;
         tc_fence_after();
         {
