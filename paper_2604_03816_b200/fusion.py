@@ -19,7 +19,8 @@ as shipped in ``pkg/src/aqsim/dag.py``:
 * passes repeat until a full sweep merges nothing (ref dag.py:177-217).
 
 Given the same input, the output gate list (order, targets, matrices) equals
-the reference's; ``tests/test_fusion.py`` pins that against golden fixtures.
+the reference's; ``tests/test_fusion.py`` pins that against the golden
+fixtures that ``tests/golden/make_golden.py`` made with ``aqsim.dag.fuse``.
 """
 from __future__ import annotations
 

@@ -20,6 +20,13 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 REFERENCE_SRC = "/root/reference/pkg/src"
+# the unmodified reference package installed by the driver's one offline
+# install (`pip install --target baseline/_ref /root/reference/pkg`); it
+# travels to the GPU box, so the drop-in tests (aqsim.run_circuit("b200"),
+# selector profiling) run there too.  Appended, never shadowing the repo.
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+if os.path.isdir(os.path.join(REFERENCE_INSTALL, "aqsim")) and REFERENCE_INSTALL not in sys.path:
+    sys.path.append(REFERENCE_INSTALL)
 
 
 def pytest_configure(config):

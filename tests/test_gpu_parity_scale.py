@@ -1,0 +1,280 @@
+"""GPU parity at BASELINE scale: the steady-state tile pipeline against the oracle.
+
+The small-n tests in ``test_gpu_parity.py`` never let a tile stream process a
+second tile (n <= 20 gives <= 256 tiles on a 148-CTA grid).  Here:
+
+* 23-qubit circuits (>= 1024 tiles, every stream refills its stage and flips
+  its barrier parity many times) on the default plans and on the stream /
+  tile-size / kernel variants, against the oracle port;
+* QFT on random adopted states (every controlled phase acts non-trivially --
+  QFT|0> is blind to them) and on basis inputs, where the exact answer is the
+  DFT of the bit-reversed input (ref pkg/tests/test_generators.py:39-50);
+* BASELINE config 3 (QFT-30, c128) at full size: the DFT closed form checked on
+  the device for a random basis input, a QFT . QFT^dagger mirror from a basis
+  state, and the first fused gates against the oracle port;
+* BASELINE config 2 (layered-28, c64) at full size against the oracle port.
+
+Tolerances are the north star's (c128 max-abs <= 1e-12, F >= 1 - 1e-10; c64
+max-abs <= 1e-5, normalised F >= 1 - 1e-5).  The oracle is test
+infrastructure: the reference's NumPy kernels, chunked over all host threads
+(``oracle.sv_oracle.apply_gate_parallel``, bit-identical to the serial port).
+"""
+from __future__ import annotations
+
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+from oracle import sv_oracle as orc
+from paper_2604_03816_b200 import generators as gen
+from paper_2604_03816_b200.b200 import B200Engine, plan_options
+from paper_2604_03816_b200.circuit import Circuit, GateKind, GateOp, Precision, effective_unitary
+from paper_2604_03816_b200.fusion import fuse
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+TOL = {"double": (1e-12, 1e-10), "single": (1e-5, 1e-5)}
+WORKERS = max(1, os.cpu_count() or 1)
+_POOL = ThreadPoolExecutor(WORKERS)
+_CACHE: dict = {}
+
+
+def oracle_run(circuit, prec: str, init: np.ndarray | None = None, key=None) -> np.ndarray:
+    """The reference kernels over all host threads (cached per key)."""
+    if key is not None and key in _CACHE:
+        return _CACHE[key]
+    n = circuit.num_qubits
+    amps = orc.init_state(n, prec) if init is None else init.astype(orc.dtype_of(prec)).copy()
+    for op in circuit.gates:
+        orc.apply_gate_parallel(amps, n, op, _POOL, WORKERS)
+    if key is not None:
+        _CACHE[key] = amps
+    return amps
+
+
+def check(got: np.ndarray, want: np.ndarray, prec: str, what: str = "") -> tuple[float, float]:
+    amax, ftol = TOL[prec]
+    g = got.astype(np.complex128)
+    w = want.astype(np.complex128)
+    err = float(np.abs(g - w).max())
+    fid = orc.normalised_fidelity(g, w)
+    assert err <= amax, f"{what} max-abs {err:.3e} > {amax}"
+    assert fid >= 1 - ftol, f"{what} fidelity 1-{1 - fid:.3e}"
+    return err, fid
+
+
+def random_state(n: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return v / np.linalg.norm(v)
+
+
+def dagger(c: Circuit) -> Circuit:
+    return Circuit(c.num_qubits, [GateOp(GateKind.CUSTOM, op.targets, (), effective_unitary(op).conj().T)
+                                  for op in reversed(c.gates)])
+
+
+def bitrev(x: int, n: int) -> int:
+    return int(format(x, f"0{n}b")[::-1], 2)
+
+
+def run_planned(eng: B200Engine, circuit, prec: str, init: np.ndarray | None = None):
+    p = Precision(prec)
+    st = eng.init_state(circuit.num_qubits, p) if init is None else eng.adopt(circuit.num_qubits, p, init)
+    plan = eng.plan(circuit, p)
+    eng.execute(st, plan)
+    return st, plan
+
+
+N_MULTI = 23
+# (options, precisions): default plans, every tile-stream count, tile sizes,
+# FFMA-only phases, warp-level mma.sync phases
+VARIANTS = [({}, ("single", "double")),
+            ({"streams": 2}, ("single", "double")),
+            ({"streams": 3}, ("single", "double")),
+            ({"streams": 4}, ("single",)),
+            ({"streams": 1}, ("single", "double")),
+            ({"tile_bits": 13}, ("single",)),
+            ({"tile_bits": 12, "streams": 2}, ("single", "double")),
+            ({"tensor_cores": -1}, ("single",)),
+            ({"tensor_cores": -1, "tile_bits": 12, "stages": 2}, ("single",)),
+            ({"tile_bits": 13, "tensor_cores": 2, "streams": 1}, ("single",))]
+CASES = [(opts, prec) for opts, precs in VARIANTS for prec in precs]
+
+
+@pytest.fixture(scope="module")
+def multi_circuits():
+    lay, rep = fuse(gen.layered_circuit(N_MULTI, seed=11), 2)
+    qft, _ = fuse(gen.qft_circuit(N_MULTI - 1), 2)
+    return {"layered": lay, "qft": qft, "init": random_state(N_MULTI - 1, 5)}
+
+
+@pytest.mark.parametrize("opts,prec", CASES, ids=[f"{p}-{o}" for o, p in CASES])
+def test_multitile_streams_vs_oracle(multi_circuits, opts, prec):
+    """>= 5 tiles per CTA per pass: stage refills, barrier parity flips and the
+    outside-tile index ring all run under an oracle check."""
+    eng = B200Engine("b200-multi", options=plan_options(**opts) if opts else None)
+    lay = multi_circuits["layered"]
+    st, plan = run_planned(eng, lay, prec)
+    for info in plan.passes():
+        assert (1 << (N_MULTI - info["tile_bits"])) >= 5 * 148
+    check(st.amplitudes, oracle_run(lay, prec, key=("layered", prec)), prec, f"layered-{N_MULTI} {opts}")
+    eng.release(st)
+    qft, init = multi_circuits["qft"], multi_circuits["init"]
+    st, _ = run_planned(eng, qft, prec, init)
+    check(st.amplitudes, oracle_run(qft, prec, init, key=("qft", prec)), prec, f"qft-{N_MULTI - 1} {opts}")
+    eng.release(st)
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+@pytest.mark.parametrize("n", [16, 20])
+def test_qft_on_random_states(n, prec):
+    """Every controlled phase of the QFT acts on a random input; fused (outside-
+    tile diagonal tables) and unfused circuits against the oracle."""
+    eng = B200Engine("b200-qft")
+    init = random_state(n, 100 + n)
+    for circ in (fuse(gen.qft_circuit(n), 2)[0], fuse(gen.qft_circuit(n), 3)[0], gen.qft_circuit(n)):
+        st, _ = run_planned(eng, circ, prec, init)
+        check(st.amplitudes, oracle_run(circ, prec, init), prec, f"qft-{n} random state")
+        eng.release(st)
+
+
+def dft_column(n: int, x: int) -> np.ndarray:
+    """DFT of the bit-reversed basis input: (1/sqrt N) exp(2 pi i j k / N), k = rev(x)."""
+    N = 1 << n
+    k = bitrev(x, n)
+    j = np.arange(N, dtype=np.int64)
+    ph = (j * k) & (N - 1)
+    return np.exp(2j * np.pi * ph / N) / math.sqrt(N)
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+@pytest.mark.parametrize("n", [16, 22])
+def test_qft_is_dft_on_basis_inputs(n, prec):
+    """GPU counterpart of ref test_generators.py:39-50: up to a global phase the
+    QFT maps |rev(k)> to the k-th DFT column."""
+    eng = B200Engine("b200-dft")
+    f, _ = fuse(gen.qft_circuit(n), 2)
+    rng = np.random.default_rng(n)
+    for x in [1, (1 << n) - 1] + [int(v) for v in rng.integers(1, 1 << n, 2)]:
+        init = np.zeros(1 << n, dtype=np.complex128)
+        init[x] = 1
+        st, _ = run_planned(eng, f, prec, init)
+        got = st.amplitudes.astype(np.complex128)
+        want = dft_column(n, x)
+        phase = got[0] / abs(got[0])  # the CP decomposition's global phase
+        check(got, phase * want, prec, f"qft-{n} |{x}>")
+        eng.release(st)
+
+
+def _device_dft_error(tensor, n: int, x: int) -> float:
+    """max |amp_j - phase e^{2 pi i j k / N} / sqrt N| over the device state, in chunks."""
+    import torch
+    N = 1 << n
+    k = bitrev(x, n)
+    a0 = complex(tensor[0].item())
+    phase = a0 / abs(a0)
+    assert abs(abs(a0) - N ** -0.5) <= 1e-12
+    worst = 0.0
+    chunk = 1 << 26
+    ph = torch.tensor(phase, dtype=torch.complex128, device=tensor.device)
+    for c0 in range(0, N, chunk):
+        j = torch.arange(c0, min(N, c0 + chunk), dtype=torch.int64, device=tensor.device)
+        ang = ((j * k) & (N - 1)).to(torch.float64) * (2 * math.pi / N)
+        want = torch.polar(torch.full_like(ang, N ** -0.5), ang) * ph
+        worst = max(worst, float((tensor[c0:c0 + chunk] - want).abs().max().item()))
+    return worst
+
+
+def _basis_state_on_device(eng, n: int, x: int, prec: Precision):
+    import torch
+    st = eng.init_state(n, prec)
+    st.tensor.zero_()
+    st.tensor[x] = 1
+    st.touch()
+    torch.cuda.synchronize()
+    return st
+
+
+def test_qft30_c128_is_dft_full_size():
+    """BASELINE config 3 at full size with a value check of every controlled
+    phase: QFT-30 of a random basis state equals the DFT column, <= 1e-12."""
+    import torch
+    eng = B200Engine("b200-qft30")
+    n = 30
+    f, rep = fuse(gen.qft_circuit(n), 2)
+    assert rep.fused_gate_count == 435
+    x = 0b101101110010101110101101001011  # 30 bits, mixed
+    st = _basis_state_on_device(eng, n, x, Precision.DOUBLE)
+    eng.execute(st, eng.plan(f, Precision.DOUBLE))
+    eng.synchronize()
+    err = _device_dft_error(st.tensor, n, x)
+    assert err <= 1e-12, err
+    assert abs(eng.norm_squared(st) - 1.0) <= 1e-10
+    eng.release(st)
+    del st
+    torch.cuda.empty_cache()
+
+
+def test_qft30_c128_mirror_from_basis_state():
+    """QFT-30 followed by its inverse returns a (non-zero) basis state."""
+    import torch
+    eng = B200Engine("b200-qft30m")
+    n = 30
+    f, _ = fuse(gen.qft_circuit(n), 2)
+    mirror = Circuit(n, list(f.gates) + list(dagger(f).gates))
+    x = (1 << 29) | (1 << 17) | 0b1011011
+    st = _basis_state_on_device(eng, n, x, Precision.DOUBLE)
+    eng.execute(st, eng.plan(mirror, Precision.DOUBLE))
+    eng.synchronize()
+    t = st.tensor
+    assert abs(complex(t[x].item()) - 1.0) <= 1e-10
+    t[x] = 0
+    assert float(t.abs().max().item()) <= 1e-12
+    eng.release(st)
+    del st, t
+    torch.cuda.empty_cache()
+
+
+def test_qft30_c128_prefix_vs_oracle():
+    """The first fused gates of BASELINE config 3 at full size against the oracle
+    port (a 16 GiB host state; the oracle runs over all host threads)."""
+    import torch
+    n, K = 30, 10
+    f, _ = fuse(gen.qft_circuit(n), 2)
+    prefix = Circuit(n, list(f.gates[:K]))
+    x = 0b110010111010010111001011101001
+    eng = B200Engine("b200-qft30p")
+    st = _basis_state_on_device(eng, n, x, Precision.DOUBLE)
+    eng.execute(st, eng.plan(prefix, Precision.DOUBLE))
+    got = st.amplitudes
+    eng.release(st)
+    del st
+    torch.cuda.empty_cache()
+    init = np.zeros(1 << n, dtype=np.complex128)
+    init[x] = 1
+    want = oracle_run(prefix, "double", init)
+    del init
+    check(got, want, "double", f"qft-30 prefix {K}")
+
+
+def test_layered28_c64_full_size_vs_oracle():
+    """BASELINE config 2 end to end against the oracle port (973 -> 189 fused
+    gates at 28 q, complex64): max-abs and normalised fidelity."""
+    import torch
+    f, rep = fuse(gen.layered_circuit(28), 2)
+    assert (rep.original_gate_count, rep.fused_gate_count) == (973, 189)
+    eng = B200Engine("b200-l28")
+    st = eng.run_circuit(f, Precision.SINGLE)
+    got = st.amplitudes
+    eng.release(st)
+    del st
+    torch.cuda.empty_cache()
+    want = oracle_run(f, "single")
+    err, fid = check(got, want, "single", "layered-28 c64")
+    print(f"layered-28 c64 full size: max-abs {err:.3e}, 1 - F {1 - fid:.3e}")
