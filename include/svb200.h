@@ -59,10 +59,11 @@ typedef struct svb_plan_options {
                            CTAs per SM of a 2-stage ring)                         */
   int reg_bits;         /* amplitudes per thread = 2^reg_bits (0: 5 for c64, 4 c128) */
   int no_reg_phases;    /* 1: force the shared-memory-per-op kernel (k_tile_pass)    */
-  int tensor_cores;     /* c64 only: 2 = fuse whole register phases into warp-level
-                           tensor-core GEMMs (mma.sync f16 hi/lo, in k_reg_pass);
-                           1 = tcgen05 TF32x3 GEMMs (k_tc_pass, 12-qubit tiles,
-                           experimental); 0 = default (2 for c64), -1 = off */
+  int tensor_cores;     /* c64 only: 0 = default = 1: passes with >= tc_min_dense dense
+                           gates run k_gemm_pass (every dense op in tcgen05 GEMMs,
+                           both operands in shared memory); 2 = tensor-core phases
+                           inside k_reg_pass (A in TMEM / warp-level mma.sync);
+                           -1 = FMA pipes only */
   int tc_min_dense;     /* dense gates a phase needs to become a GEMM (0: 2)         */
   int no_window_search; /* 1: plain program-order greedy pass building             */
   int streams;          /* tile streams per CTA for register phases: 2..4 = warp
@@ -83,7 +84,17 @@ typedef struct svb_pass_info {
   int reg_bits;         /* > 0: register-phase kernel with 2^reg_bits amps per thread */
   int num_phases;       /* register phases (0 for the shared-memory kernel) */
   int num_tc;           /* phases executed as tensor-core GEMMs */
+  int kernel;           /* SVB_KERNEL_TILE / _REG / _REG_TC / _GEMM */
+  int streams;          /* tile streams per CTA (warp groups of 128 threads) */
+  int bank_conflicts;   /* k_gemm_pass: sum of log2 bank-conflict degrees of the A writes */
 } svb_pass_info;
+
+enum {
+  SVB_KERNEL_TILE = 0,   /* k_tile_pass: shared-memory ops                         */
+  SVB_KERNEL_REG = 1,    /* k_reg_pass: register phases on the FMA pipes            */
+  SVB_KERNEL_REG_TC = 2, /* k_reg_pass with tensor-core phases (A in TMEM / mma.sync) */
+  SVB_KERNEL_GEMM = 3    /* k_gemm_pass: tcgen05 GEMMs, both operands in shared memory */
+};
 
 int svb_abi_version(void);
 const char* svb_last_error(void);
@@ -149,6 +160,9 @@ void svb_plan_destroy(svb_plan* plan);
  * (ref engines.py:340-346).  Results are written to host memory; the call
  * synchronises `stream`.  out2 = {re, im} of sum conj(a[i]) * b[i]. */
 int svb_dot(const void* a, const void* b, int n_local, int prec, double* out2, void* stream);
+/* <a|b> with a and b in possibly different precisions, both promoted to
+   complex128 as ref engines.py:340-346 (state_fidelity) does. */
+int svb_dot_mixed(const void* a, int prec_a, const void* b, int prec_b, int n_local, double* out2, void* stream);
 int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream);
 
 /* |amp|^2 as float64 -- replaces StateVector.probabilities (ref circuit.py:203-205)

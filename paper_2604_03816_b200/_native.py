@@ -25,7 +25,7 @@ EXPORTS = (
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
     "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext", "svb_plan_phase_map",
     "svb_plan_execute",
-    "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_norm2",
+    "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_dot_mixed", "svb_norm2",
     "svb_probabilities", "svb_block_sums", "svb_sample_search",
 )
 
@@ -42,7 +42,11 @@ class PassInfo(C.Structure):
     _fields_ = [("tile_bits", C.c_int), ("low_bits", C.c_int), ("num_high", C.c_int),
                 ("high", C.c_int * 8), ("num_kernel_ops", C.c_int), ("num_gates", C.c_int),
                 ("est_cost", C.c_double), ("reg_bits", C.c_int), ("num_phases", C.c_int),
-                ("num_tc", C.c_int)]
+                ("num_tc", C.c_int), ("kernel", C.c_int), ("streams", C.c_int),
+                ("bank_conflicts", C.c_int)]
+
+
+KERNELS = ("tile", "reg", "reg_tc", "gemm")
 
 
 class NativeError(RuntimeError):
@@ -87,6 +91,7 @@ def lib():
         "svb_plan_execute_range": (i, [vp, vp, i, i, vp]),
         "svb_plan_destroy": (None, [vp]),
         "svb_dot": (i, [vp, vp, i, i, dp, vp]),
+        "svb_dot_mixed": (i, [vp, i, vp, i, i, dp, vp]),
         "svb_norm2": (i, [vp, i, i, dp, vp]),
         "svb_probabilities": (i, [vp, i, ll, ll, vp, vp]),
         "svb_block_sums": (i, [vp, i, i, i, vp, vp]),
@@ -151,7 +156,8 @@ class NativePlan:
                 "high": [info.high[b] for b in range(info.num_high)],
                 "num_kernel_ops": info.num_kernel_ops, "num_gates": info.num_gates,
                 "est_cost": info.est_cost, "reg_bits": info.reg_bits, "num_phases": info.num_phases,
-                "num_tc": info.num_tc}
+                "num_tc": info.num_tc, "kernel": KERNELS[info.kernel], "streams": info.streams,
+                "bank_conflicts": info.bank_conflicts}
 
     def phase(self, p: int, f: int) -> dict:
         R = (C.c_int * 8)()

@@ -274,13 +274,12 @@ class B200Engine(EngineBase):
         """<a|b> accumulated in FP64 on the device."""
         if a.num_qubits != b.num_qubits:
             raise ValueError(f"qubit counts differ: {a.num_qubits} vs {b.num_qubits}")
-        if prec_code(a.precision) != prec_code(b.precision):
-            b = self.adopt(b.num_qubits, a.precision, b.tensor)
-            self.live_states -= 1
+        # mixed precisions: both promoted to complex128 in the kernel (ref
+        # engines.py:340-346), no copy of either state
         out = (C.c_double * 2)()
-        _native.check(_native.lib().svb_dot(C.c_void_p(a.tensor.data_ptr()),
-                                            C.c_void_p(b.tensor.data_ptr()), a.num_qubits,
-                                            prec_code(a.precision), out, C.c_void_p(self.stream())))
+        _native.check(_native.lib().svb_dot_mixed(
+            C.c_void_p(a.tensor.data_ptr()), prec_code(a.precision), C.c_void_p(b.tensor.data_ptr()),
+            prec_code(b.precision), a.num_qubits, out, C.c_void_p(self.stream())))
         return complex(out[0], out[1])
 
     def fidelity(self, a: DeviceStateVector, b: DeviceStateVector, normalised: bool = False) -> float:

@@ -11,9 +11,6 @@ namespace svb {
 // Measured on B200 (profiles/r01_*): c64 passes are FFMA-issue bound, so the
 // widest register tile (13 qubits, 32 amplitudes per thread) wins; c128 uses
 // 11-qubit tiles with 8 amplitudes per thread (FP64 register pressure).
-constexpr int kMaxTcPerPass = 2;        // fused GEMM matrices per pass (shared memory)
-constexpr double kTcDenseCost = 0.15;   // planner cost of a dense gate in a tensor-core pass
-constexpr double kTcDefaultBudget = 3.0;
 
 // c128: 12-qubit tiles with 16 amplitudes per thread at 1 CTA/SM (measured
 // layered-30 450 ms vs 513 ms for 11-qubit tiles x 8 amplitudes at 2 CTAs/SM:
@@ -37,17 +34,14 @@ namespace {
 // the summed op cost stays below 1.0 (the default budget).
 struct CostModel {
   double s, fma, mem;
-  bool tc;
-  explicit CostModel(int prec, bool tensor = false) {
+  explicit CostModel(int prec) {
     s = prec == SVB_C64 ? 8.0 : 16.0;
     fma = prec == SVB_C64 ? 128.0 : 64.0;
     mem = 2.0 * s / 23.0;
-    tc = tensor;
   }
   // register-resident ops: FMAs plus, amortised, half a shared-memory
   // transpose per dense op (phases hold ~2 dense ops)
   double dense(int k) const {
-    if (tc) return kTcDenseCost;  // amortised share of a fused tensor-core phase
     double flops = 4.0 * double(1 << k) / fma;
     double smem = 0.5 * 2.0 * s / 128.0;
     return (flops * 1.2 + smem) / mem;
@@ -407,83 +401,6 @@ std::vector<cd> reg_op_matrix(const RegOp& ro, int RB) {
   return m;
 }
 
-// Fold, in up to max_tc phases, the longest run of register-only ops (dense
-// ops, and diagonal ops without thread-sourced bits) with >= min_dense dense
-// ops into one matrix product executed as a tensor-core GEMM (k_tc_pass).
-void fuse_tc_phases(Pass& p, int min_dense, int max_tc) {
-  const int RB = p.reg_bits;
-  const int D = 1 << RB;
-  struct Cand { int dense, phase, a, c; };
-  std::vector<Cand> cands;
-  for (int f = 0; f < int(p.phases.size()); ++f) {
-    const RegPhase& ph = p.phases[f];
-    int best = -1, ba = 0, bc = 0;
-    for (int a = ph.op_begin; a < ph.op_end;) {
-      int c = a, dense = 0;
-      while (c < ph.op_end &&
-             (p.reg_ops[c].kind == OP_DENSE || (p.reg_ops[c].mask == 0 && p.reg_ops[c].kx == 0))) {
-        dense += p.reg_ops[c].kind == OP_DENSE;
-        ++c;
-      }
-      if (c > a && dense > best) {
-        best = dense;
-        ba = a;
-        bc = c;
-      }
-      a = c > a ? c : a + 1;
-    }
-    if (best >= min_dense) cands.push_back({best, f, ba, bc});
-  }
-  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {
-    return x.dense != y.dense ? x.dense > y.dense : x.phase < y.phase;
-  });
-  if (int(cands.size()) > max_tc) cands.resize(max_tc);
-  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) { return x.phase < y.phase; });
-  std::vector<KernelOp> ops;
-  std::vector<RegOp> rops;
-  size_t ci = 0;
-  p.tc_mats.clear();
-  for (int f = 0; f < int(p.phases.size()); ++f) {
-    RegPhase& ph = p.phases[f];
-    const int b = ph.op_begin, e = ph.op_end;
-    const bool fuse = ci < cands.size() && cands[ci].phase == f;
-    const int a = fuse ? cands[ci].a : e, c = fuse ? cands[ci].c : e;
-    ph.op_begin = int(ops.size());
-    for (int i = b; i < a; ++i) {
-      ops.push_back(p.ops[i]);
-      rops.push_back(p.reg_ops[i]);
-    }
-    ph.op_mid = int(ops.size());
-    if (fuse) {
-      std::vector<cd> U(size_t(D) * D, cd());
-      for (int r = 0; r < D; ++r) U[size_t(r) * D + r] = 1.0;
-      for (int i = a; i < c; ++i) {
-        const std::vector<cd> M = reg_op_matrix(p.reg_ops[i], RB);
-        std::vector<cd> nu(size_t(D) * D, cd());
-        for (int r = 0; r < D; ++r)
-          for (int q = 0; q < D; ++q) {
-            const cd mrq = M[size_t(r) * D + q];
-            if (mrq == cd()) continue;
-            for (int s = 0; s < D; ++s) nu[size_t(r) * D + s] += mrq * U[size_t(q) * D + s];
-          }
-        U.swap(nu);
-        for (int g : p.ops[i].gates) ph.tc_gates.push_back(g);
-      }
-      ph.tc = int(p.tc_mats.size());
-      p.tc_mats.push_back(std::move(U));
-      ++ci;
-    }
-    for (int i = c; i < e; ++i) {
-      ops.push_back(p.ops[i]);
-      rops.push_back(p.reg_ops[i]);
-    }
-    ph.op_end = int(ops.size());
-  }
-  p.ops.swap(ops);
-  p.reg_ops.swap(rops);
-  p.tensor_cores = true;
-}
-
 // Turn up to max_mma whole register phases (c64, RB 5, 8 thread bits) whose
 // ops all act on register bits only into one fused 32x32 matrix each,
 // executed by k_reg_pass as a warp-level tensor-core GEMM (mma.sync m16n8k16,
@@ -623,6 +540,390 @@ void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
   p.renorm = ok;
 }
 
+// ------------------------------------------------------------ k_gemm_pass
+// A-operand word of each tile bit in a phase layout (register bits j0..j4 =
+// map[0..4], row bits m0..m6 = map[5..11]); word = m 32 + ((j >> 2) ^ (m & 7)) 4
+// + (j & 3), the K-major SWIZZLE_128B canonical layout of svb_gemmpass.cuh.
+void gemm_word_table(const int* map, unsigned short* wt) {
+  static const unsigned short jw[5] = {1, 2, 4, 8, 16};
+  static const unsigned short mw[7] = {32 | 4, 64 | 8, 128 | 16, 256, 512, 1024, 2048};
+  for (int i = 0; i < 16; ++i) wt[i] = 0;
+  for (int i = 0; i < 5; ++i) wt[map[i]] = jw[i];
+  for (int b = 0; b < 7; ++b) wt[map[5 + b]] = mw[b];
+}
+
+int gf2_rank(std::vector<int> v) {
+  int r = 0;
+  for (int bit = 31; bit >= 0; --bit) {
+    int piv = -1;
+    for (size_t i = r; i < v.size(); ++i)
+      if ((v[i] >> bit) & 1) {
+        piv = int(i);
+        break;
+      }
+    if (piv < 0) continue;
+    std::swap(v[r], v[piv]);
+    for (size_t i = 0; i < v.size(); ++i)
+      if (int(i) != r && ((v[i] >> bit) & 1)) v[i] ^= v[r];
+    ++r;
+  }
+  return r;
+}
+
+// log2 of the bank-conflict degree when the lanes of layout `cur` (tile bits
+// cur[5..9]) store 4-byte words into the A operand laid out by `nxt`
+int gemm_write_conflict(const int* cur, const int* nxt) {
+  unsigned short wt[16];
+  gemm_word_table(nxt, wt);
+  std::vector<int> v;
+  for (int b = 0; b < 5; ++b) v.push_back(wt[cur[5 + b]] & 31);
+  return 5 - gf2_rank(v);
+}
+
+// log2 of the extra 128-B segments of 8-byte accesses whose lanes are tile
+// bits lanes[0..4] of the linear tile (coalesced loads / stores need the four
+// lowest tile bits -- 16 amplitudes = 128 B -- on the lanes)
+int linear_lane_cost(const int* lanes) {
+  std::vector<int> v;
+  for (int b = 0; b < 5; ++b) v.push_back(lanes[b] < 4 ? (1 << lanes[b]) : 0);
+  return 4 - gf2_rank(v);
+}
+
+// Layout of GEMM phase f given the lanes of the previous layout: the previous
+// lanes that are register bits of f go to j0, j1 (bank bits 0, 1) and then to
+// j2..j4, those that are row bits to m0..m2 (bank bits 2..4 -- XOR-paired
+// with j2..j4, so a pair never shares a bank bit); the other lane positions
+// take row bits the next boundary wants (`pref`, in order).
+void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pref, int* map) {
+  const int T = kGemmTileBits;
+  std::vector<int> inR(T, 0);
+  for (int i = 0; i < 5; ++i) inR[R[i]] = 1;
+  std::vector<int> X, Y;
+  for (int b = 0; b < 5; ++b) (inR[prev_lanes[b]] ? X : Y).push_back(prev_lanes[b]);
+  int j[5] = {-1, -1, -1, -1, -1}, m[7] = {-1, -1, -1, -1, -1, -1, -1};
+  bool slot_used[3] = {false, false, false};  // bank bits 2..4
+  size_t xi = 0;
+  for (int s = 0; s < 2 && xi < X.size(); ++s) j[s] = X[xi++];
+  for (size_t yi = 0; yi < Y.size() && yi < 3; ++yi) {
+    m[yi] = Y[yi];
+    slot_used[yi] = true;
+  }
+  for (int s = 0; s < 3 && xi < X.size(); ++s)
+    if (!slot_used[s]) {
+      j[2 + s] = X[xi++];
+      slot_used[s] = true;
+    }
+  std::vector<int> used(T, 0);
+  for (int i = 0; i < 5; ++i)
+    if (j[i] >= 0) used[j[i]] = 1;
+  for (int i = 0; i < 7; ++i)
+    if (m[i] >= 0) used[m[i]] = 1;
+  // leftovers of the previous lanes (conflicting) first, then the rest
+  for (int i = 0; i < 5; ++i)
+    if (j[i] < 0)
+      for (int t : X)
+        if (!used[t]) {
+          j[i] = t;
+          used[t] = 1;
+          break;
+        }
+  for (int i = 0; i < 5; ++i)
+    if (j[i] < 0)
+      for (int q = 0; q < 5; ++q)
+        if (!used[R[q]]) {
+          j[i] = R[q];
+          used[R[q]] = 1;
+          break;
+        }
+  for (size_t yi = 3; yi < Y.size(); ++yi)
+    for (int i = 0; i < 7; ++i)
+      if (m[i] < 0) {
+        m[i] = Y[yi];
+        used[Y[yi]] = 1;
+        break;
+      }
+  for (int i = 0; i < 7; ++i) {
+    if (m[i] >= 0) continue;
+    int pick = -1;
+    if (i < 5)
+      for (int t : pref)
+        if (!used[t] && !inR[t]) {
+          pick = t;
+          break;
+        }
+    if (pick < 0)
+      for (int t = 0; t < T; ++t)
+        if (!used[t] && !inR[t]) {
+          pick = t;
+          break;
+        }
+    m[i] = pick;
+    used[pick] = 1;
+  }
+  for (int i = 0; i < 5; ++i) map[i] = j[i];
+  for (int b = 0; b < 7; ++b) map[5 + b] = m[b];
+}
+
+// Lower a pass (12-qubit tile, unitary ops) for k_gemm_pass: list-schedule
+// register phases (build_phases), fold each phase's dense ops and register-
+// only diagonal ops into one 32x32 matrix, move diagonal ops on row / outside
+// bits before or after the GEMM they commute with, and choose every phase's
+// qubit order for conflict-free A writes and coalesced loads / stores.
+// Returns false (pass left unchanged) when the pass does not fit the kernel.
+bool build_gemm_pass(Pass& p) {
+  const int T = kGemmTileBits;
+  if (p.T != T) return false;
+  for (const KernelOp& op : p.ops) {  // unitary ops only (the kernel rescales by the tile norm)
+    const int d = 1 << op.k;
+    if (op.kind == OP_DIAG) {
+      for (const cd& z : op.coeff)
+        if (std::abs(std::abs(z) - 1.0) > 1e-9) return false;
+      continue;
+    }
+    for (int r = 0; r < d; ++r)
+      for (int t = 0; t < d; ++t) {
+        cd acc = 0.0;
+        for (int q = 0; q < d; ++q) acc += std::conj(op.coeff[size_t(q) * d + r]) * op.coeff[size_t(q) * d + t];
+        if (std::abs(acc - (r == t ? cd(1.0) : cd(0.0))) > 1e-9) return false;
+      }
+  }
+  Pass q = p;
+  if (!build_phases(q, 5, SVB_C64, 7)) return false;
+  struct GP {
+    int R[5];
+    std::vector<cd> U;  // ascending-R index space
+    std::vector<int> post, gates;
+  };
+  std::vector<int> pre0;
+  std::vector<GP> gps;
+  const int D = 32;
+  auto bits_of = [&](const KernelOp& op) {
+    unsigned long long b = 0;  // tile bits 0..T-1, outside-tile qubits at T + q
+    for (int j = 0; j < op.k; ++j) b |= 1ULL << std::min(op.tgt[j], 63);
+    return b;
+  };
+  for (const RegPhase& ph : q.phases) {
+    const int* R = ph.R;
+    int rmask = 0;
+    for (int i = 0; i < 5; ++i) rmask |= 1 << R[i];
+    auto rpos = [&](int t) {
+      for (int i = 0; i < 5; ++i)
+        if (R[i] == t) return i;
+      return -1;
+    };
+    std::vector<unsigned long long> dense_bits;
+    for (int i = ph.op_begin; i < ph.op_end; ++i)
+      dense_bits.push_back(q.ops[i].kind == OP_DENSE ? bits_of(q.ops[i]) : 0ULL);
+    bool any_dense = false;
+    for (auto b : dense_bits) any_dense = any_dense || b;
+    if (!any_dense) {
+      for (int i = ph.op_begin; i < ph.op_end; ++i) (gps.empty() ? pre0 : gps.back().post).push_back(i);
+      continue;
+    }
+    GP g;
+    for (int i = 0; i < 5; ++i) g.R[i] = R[i];
+    g.U.assign(size_t(D) * D, cd());
+    for (int r = 0; r < D; ++r) g.U[size_t(r) * D + r] = 1.0;
+    std::vector<int> pre;
+    for (int i = ph.op_begin; i < ph.op_end; ++i) {
+      const KernelOp& op = q.ops[i];
+      const unsigned long long b = bits_of(op);
+      const bool reg_only = (b & ~(unsigned long long)rmask) == 0;
+      if (op.kind == OP_DIAG && !reg_only) {
+        unsigned long long before = 0, after = 0;
+        for (int k = ph.op_begin; k < ph.op_end; ++k)
+          (k < i ? before : after) |= k == i ? 0ULL : dense_bits[k - ph.op_begin];
+        if ((b & after) == 0) {
+          g.post.push_back(i);
+        } else if ((b & before) == 0) {
+          pre.push_back(i);
+        } else {
+          return false;
+        }
+        continue;
+      }
+      // fold into U: M (in ascending-R index space) times U
+      int pos[kMaxK];
+      for (int j = 0; j < op.k; ++j) pos[j] = rpos(op.tgt[j]);
+      std::vector<cd> nu(size_t(D) * D, cd());
+      const int d = 1 << op.k;
+      int omask = 0;
+      for (int j = 0; j < op.k; ++j) omask |= 1 << pos[j];
+      for (int r = 0; r < D; ++r) {
+        int a = 0;
+        for (int j = 0; j < op.k; ++j) a |= ((r >> pos[j]) & 1) << j;
+        for (int bb = 0; bb < d; ++bb) {
+          cd mrb;
+          if (op.kind == OP_DIAG) {
+            if (bb != a) continue;
+            mrb = op.coeff[a];
+          } else {
+            mrb = op.coeff[size_t(a) * d + bb];
+          }
+          if (mrb == cd()) continue;
+          int c = r & ~omask;
+          for (int j = 0; j < op.k; ++j) c |= ((bb >> j) & 1) << pos[j];
+          for (int s = 0; s < D; ++s) nu[size_t(r) * D + s] += mrb * g.U[size_t(c) * D + s];
+        }
+      }
+      g.U.swap(nu);
+      for (int gi : op.gates) g.gates.push_back(gi);
+    }
+    for (int i : pre) (gps.empty() ? pre0 : gps.back().post).push_back(i);
+    gps.push_back(std::move(g));
+  }
+  const int P = int(gps.size());
+  if (P < 1 || P > kMaxMmaPerPass || P + 1 > kMaxPhases) return false;
+
+  // ---- layouts: choose the load lanes, then each GEMM phase greedily
+  std::vector<std::vector<int>> maps(P + 1, std::vector<int>(16, 0));
+  auto pref_for = [&](int f) {  // row bits phase f's lanes should carry
+    std::vector<int> pr;
+    if (f < P) {
+      for (int i = 0; i < 5; ++i) pr.push_back(gps[f].R[i]);  // gps[f] is GEMM phase f + 1
+    } else {
+      for (int t = 0; t < 4; ++t) pr.push_back(t);  // coalesced stores
+    }
+    return pr;
+  };
+  int best_cost = 1 << 30;
+  std::vector<std::vector<int>> best;
+  std::vector<int> sel(5);
+  for (int a = 0; a < T; ++a)
+    for (int b = a + 1; b < T; ++b)
+      for (int c = b + 1; c < T; ++c)
+        for (int d = c + 1; d < T; ++d)
+          for (int e = d + 1; e < T; ++e) {
+            const int lanes[5] = {a, b, c, d, e};
+            std::vector<std::vector<int>> mp(P + 1, std::vector<int>(16, 0));
+            // load layout: lanes, then registers, then the two warp bits
+            std::vector<int> rest;
+            for (int t = 0; t < T; ++t)
+              if (t != a && t != b && t != c && t != d && t != e) rest.push_back(t);
+            for (int i = 0; i < 5; ++i) mp[0][i] = rest[i];
+            for (int i = 0; i < 5; ++i) mp[0][5 + i] = lanes[i];
+            mp[0][10] = rest[5];
+            mp[0][11] = rest[6];
+            int cost = linear_lane_cost(lanes);
+            for (int f = 1; f <= P; ++f) {
+              gemm_layout(&mp[f - 1][5], gps[f - 1].R, pref_for(f), mp[f].data());
+              cost += 2 * gemm_write_conflict(mp[f - 1].data(), mp[f].data());
+            }
+            cost += 2 * linear_lane_cost(&mp[P][5]);
+            if (cost < best_cost) {
+              best_cost = cost;
+              best = mp;
+            }
+          }
+  maps = best;
+  int conflicts = 0;
+  for (int f = 1; f <= P; ++f) conflicts += gemm_write_conflict(maps[f - 1].data(), maps[f].data());
+
+  // ---- assemble: ops in execution order, phases, GEMM matrices in layout order
+  std::vector<int> order;
+  std::vector<std::pair<int, int>> ranges;
+  ranges.push_back({0, int(pre0.size())});
+  for (int i : pre0) order.push_back(i);
+  for (int f = 0; f < P; ++f) {
+    const int b0 = int(order.size());
+    for (int i : gps[f].post) order.push_back(i);
+    ranges.push_back({b0, int(order.size())});
+  }
+  std::vector<KernelOp> ops;
+  for (int i : order) ops.push_back(q.ops[i]);
+  p.ops.swap(ops);
+  p.reg_ops.assign(p.ops.size(), RegOp());
+  p.phases.clear();
+  p.tc_mats.clear();
+  for (int f = 0; f <= P; ++f) {
+    RegPhase rp;
+    const int* mp = maps[f].data();
+    for (int i = 0; i < 16; ++i) rp.map[i] = i < T ? mp[i] : 0;
+    for (int i = 0; i < 5; ++i) rp.R[i] = mp[i];
+    rp.op_begin = ranges[f].first;
+    rp.op_end = ranges[f].second;
+    if (f == 0) {
+      rp.op_mid = rp.op_end;  // ops before any GEMM
+      rp.tc = -1;
+    } else {
+      rp.op_mid = rp.op_begin;  // GEMM first, then the diagonal ops
+      rp.tc = f - 1;
+      gemm_word_table(mp, rp.wt);
+      rp.tc_gates = gps[f - 1].gates;
+      // U in the layout's register order: register bit i <-> tile bit mp[i]
+      const int* R = gps[f - 1].R;
+      int to_asc[5];
+      for (int i = 0; i < 5; ++i)
+        for (int k = 0; k < 5; ++k)
+          if (R[k] == mp[i]) to_asc[i] = k;
+      auto conv = [&](int x) {
+        int y = 0;
+        for (int i = 0; i < 5; ++i) y |= ((x >> i) & 1) << to_asc[i];
+        return y;
+      };
+      std::vector<cd> U(size_t(D) * D);
+      for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) U[size_t(r) * D + c] = gps[f - 1].U[size_t(conv(r)) * D + conv(c)];
+      p.tc_mats.push_back(std::move(U));
+    }
+    // diagonal ops in this layout: table index = [thread bits | register bits | outside bits]
+    for (int i = rp.op_begin; i < rp.op_end; ++i) {
+      const KernelOp& op = p.ops[i];
+      RegOp& ro = p.reg_ops[i];
+      ro.kind = op.kind;
+      ro.k = op.k;
+      std::vector<std::pair<int, int>> regb, thrb, extb;
+      for (int b = 0; b < op.k; ++b) {
+        const int t = op.tgt[b];
+        if (t >= T) {
+          extb.push_back({t - T, b});
+          continue;
+        }
+        int where = -1;
+        for (int k = 0; k < T; ++k)
+          if (mp[k] == t) where = k;
+        if (where < 5)
+          regb.push_back({where, b});
+        else
+          thrb.push_back({where - 5, b});
+      }
+      std::sort(regb.begin(), regb.end());
+      std::sort(thrb.begin(), thrb.end());
+      std::sort(extb.begin(), extb.end());
+      const int kr = int(regb.size()), kt = int(thrb.size()), kx = int(extb.size());
+      ro.mask = kt;
+      for (int j = 0; j < kt; ++j) ro.src[j] = thrb[j].first;
+      ro.rmask = 0;
+      for (int j = 0; j < kr; ++j) ro.rmask |= 1 << regb[j].first;
+      ro.kx = kx;
+      ro.xmask = 0;
+      for (int j = 0; j < kx; ++j) ro.xmask |= 1ULL << extb[j].first;
+      for (int rho = 0; rho < 32; ++rho) {
+        int d = 0;
+        for (int j = 0; j < kr; ++j) d |= ((rho >> regb[j].first) & 1) << (kt + j);
+        ro.rmap[rho] = static_cast<unsigned char>(d);
+      }
+      ro.coeff.assign(op.coeff.size(), cd());
+      for (size_t nidx = 0; nidx < op.coeff.size(); ++nidx) {
+        int old = 0;
+        for (int j = 0; j < kt; ++j) old |= ((int(nidx) >> j) & 1) << thrb[j].second;
+        for (int j = 0; j < kr; ++j) old |= ((int(nidx) >> (kt + j)) & 1) << regb[j].second;
+        for (int j = 0; j < kx; ++j) old |= ((int(nidx) >> (kr + kt + j)) & 1) << extb[j].second;
+        ro.coeff[nidx] = op.coeff[old];
+      }
+    }
+    p.phases.push_back(rp);
+  }
+  p.reg_bits = 5;
+  p.thread_bits = 7;
+  p.streams = 4;
+  p.gemm = true;
+  p.mma_phases = false;
+  p.renorm = true;
+  p.bank_conflicts = conflicts;
+  return true;
+}
+
 }  // namespace
 
 // Decide the TMA tensor-map shape of a pass and the tile-local order of its
@@ -756,19 +1057,20 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     return false;
   }
   svb_plan_options opt = opt_in;
-  // tensor-core register phases (opt-in): c64 only, 12-qubit tiles (128 rows x 32 amps)
-  // tensor_cores == 2: warp-level mma.sync GEMM phases inside k_reg_pass (c64)
-  // (default for c64: measured layered-28 46 ms vs 55 ms on the FMA pipes)
-  const bool use_mma = prec == SVB_C64 && (opt.tensor_cores == 2 || opt.tensor_cores == 0) &&
-                       !opt.no_reg_phases &&
+  // c64 tensor cores (default): passes with >= 2 dense gates run on
+  // k_gemm_pass (every dense op in tcgen05 GEMMs with shared-memory operands);
+  // tensor_cores == 2: the k_reg_pass tensor-core phases (tcgen05 with A in
+  // TMEM on 12-qubit tiles, warp-level mma.sync on 13-qubit tiles);
+  // tensor_cores == -1: FMA pipes only
+  const bool use_gemm = prec == SVB_C64 && (opt.tensor_cores == 0 || opt.tensor_cores == 1) &&
+                        !opt.no_reg_phases && (opt.tile_bits == 0 || opt.tile_bits == kGemmTileBits) &&
+                        (opt.reg_bits == 0 || opt.reg_bits == 5) && opt.streams != 1;
+  const bool use_mma = prec == SVB_C64 && opt.tensor_cores >= 0 && !opt.no_reg_phases &&
                        (opt.reg_bits == 0 || opt.reg_bits == 5);
-  const bool use_tc = prec == SVB_C64 && opt.tensor_cores == 1 && !opt.no_reg_phases &&
-                      (opt.tile_bits == 0 || opt.tile_bits == 12) && (opt.reg_bits == 0 || opt.reg_bits == 5);
-  // c64 tensor-core phases: 12-qubit tiles in two warp-group streams with
-  // tcgen05 GEMMs (measured layered-28 33.2 ms vs 43.3 ms for 13-qubit tiles
-  // with mma.sync phases)
+  // c64 tensor-core phases: 12-qubit tiles in warp-group streams (measured
+  // layered-28 33.2 ms vs 43.3 ms for 13-qubit tiles with mma.sync phases)
   int T = opt.tile_bits > 0 ? opt.tile_bits
-          : ((use_tc || (use_mma && opt.streams != 1)) ? 12
+          : ((use_gemm || (use_mma && opt.streams != 1)) ? 12
              : (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4)) ? 11
                                                                                                 : default_tile_bits(prec));
   // 64 KiB tiles at most (two-stage TMA ring must fit shared memory)
@@ -782,9 +1084,9 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
                           ? opt.max_ops_per_pass : kMaxOps;
   const double budget =
-      opt.cost_budget == 0.0 ? (use_tc ? kTcDefaultBudget : default_cost_budget(prec)) : opt.cost_budget;
+      opt.cost_budget == 0.0 ? default_cost_budget(prec) : opt.cost_budget;
   const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
-  const CostModel cm(prec, use_tc);
+  const CostModel cm(prec);
 
   plan.n = n;
   plan.prec = prec;
@@ -1005,8 +1307,11 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     }
     p.ops = std::move(ops);
     p.num_gates = int(taken.size());
-    if (use_tc && p.T == 12 && build_phases(p, 5, prec, 7)) {
-      fuse_tc_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxTcPerPass);
+    int n_dense = 0;
+    for (const KernelOp& o : p.ops) n_dense += o.kind == OP_DENSE;
+    const int min_dense = opt.tc_min_dense > 0 ? opt.tc_min_dense : 2;
+    if (use_gemm && p.T == kGemmTileBits && n_dense >= min_dense && build_gemm_pass(p)) {
+      // k_gemm_pass (lowered above)
     } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
       // 12-qubit tiles: warp groups with their own tile streams (k_reg_pass TB 7)
       fuse_mma_phases(p, opt.tc_min_dense > 0 ? opt.tc_min_dense : 2, kMaxMmaPerPass, prec);

@@ -41,7 +41,7 @@ struct RegPhase {
   int R[8] = {0};           // register bit i <-> tile-local bit R[i] (ascending)
   int op_begin = 0, op_end = 0;
   int flags = 0;
-  // tensor-core phases (k_tc_pass): ops [op_begin, op_mid) run on CUDA cores,
+  // tensor-core phases: ops [op_begin, op_mid) run on CUDA cores,
   // then the fused 2^RB x 2^RB matrix tc_mats[tc] as one tcgen05 GEMM, then
   // ops [op_mid, op_end).  tc < 0: no GEMM (op_mid == op_end).
   int op_mid = 0;
@@ -50,6 +50,9 @@ struct RegPhase {
   // thread-local layout (see PhaseDesc::map); filled by build_phases
   int map[16] = {0};
   bool mma = false;           // k_reg_pass mma.sync GEMM phase (whole phase = tc_mats[tc])
+  // k_gemm_pass: word address (in the A operand of this phase's GEMM) of each
+  // tile bit, see svb_gemmpass.cuh; phase 0 (the load layout) has none
+  unsigned short wt[16] = {0};
 };
 struct RegOp {
   int kind = OP_DENSE;
@@ -78,11 +81,14 @@ struct Pass {
   int tma_start[5] = {0}, tma_bits[5] = {0}, tma_box[5] = {0};
   int n_enum = 0;
   int reg_bits = 0;               // > 0: executed by k_reg_pass<RB = reg_bits>
-  int thread_bits = 8;            // tile bits carried by the thread index (7 for k_tc_pass)
-  bool tensor_cores = false;      // executed by k_tc_pass
+  int thread_bits = 8;            // tile bits carried by the thread index (7: warp-group streams)
   bool mma_phases = false;        // k_reg_pass with mma.sync GEMM phases (tc_mats)
   bool renorm = false;            // all ops unitary: the kernel restores each tile's norm
   int streams = 1;                // tile streams per CTA (7 thread bits: 2 or 3)
+  // k_gemm_pass (c64): phases[0] = load layout + ops before the first GEMM,
+  // phases[f >= 1] = GEMM tc_mats[f - 1] then element-wise diagonal ops
+  bool gemm = false;
+  int bank_conflicts = 0;         // sum over A writes of log2(bank-conflict degree)
   std::vector<std::vector<cd>> tc_mats;  // fused phase matrices (2^RB x 2^RB, row-major)
   std::vector<RegPhase> phases;
   std::vector<RegOp> reg_ops;     // same order as ops

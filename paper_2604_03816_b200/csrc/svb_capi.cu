@@ -21,7 +21,7 @@
 #include "svb200.h"
 #include "svb_kernels.cuh"
 #include "svb_regpass.cuh"
-#include "svb_tcpass.cuh"
+#include "svb_instances.h"
 
 using namespace svb;
 
@@ -76,7 +76,8 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
-                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_tc_pass,
+                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4>,
+                         (const void*)k_gemm_pass<3>,          (const void*)k_gemm_pass<2>,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
                          (const void*)k_reg_pass<float2, 5, 7, 4>,
@@ -132,11 +133,13 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.stages = stages;
   a.h.n_phases = int(p.phases.size());
   a.h.reg_bits = p.reg_bits;
-  a.h.tc_count = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
+  a.h.tc_count = (p.mma_phases || p.gemm) ? int(p.tc_mats.size()) : 0;
   a.h.mma_phases = p.mma_phases ? 1 : 0;
   a.h.thread_bits = p.phases.empty() ? 8 : p.thread_bits;
   a.h.streams = p.phases.empty() ? 1 : p.streams;
   a.h.renorm = p.renorm ? 1 : 0;
+  a.h.gemm = p.gemm ? 1 : 0;
+  if (p.gemm) a.h.tc_count = int(p.tc_mats.size());
   a.h.tc_mats = nullptr;
   int off = 0;
   if (!p.phases.empty()) {
@@ -149,6 +152,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       d.tc = p.phases[f].tc;
       d.flags = p.phases[f].flags;
       for (int i = 0; i < 8; ++i) d.R[i] = p.phases[f].R[i];
+      if (p.gemm) std::memcpy(d.R, p.phases[f].wt, sizeof(d.R));  // A word table (16 x u16)
       for (int i = 0; i < 16; ++i) d.map[i] = static_cast<unsigned char>(p.phases[f].map[i]);
     }
     for (size_t i = 0; i < p.reg_ops.size(); ++i) {
@@ -214,6 +218,9 @@ struct svb_plan {
   std::vector<size_t> tc_offset;  // per pass, in floats
   float* tc_dev = nullptr;
   int tc_dev_id = -1;
+  // execute_range writes the launch-time fields (tensor map of the state, TMA
+  // ring depth) into the cached parameter blocks: one launcher at a time
+  std::mutex mu;
   ~svb_plan() {
     if (tc_dev) cudaFree(tc_dev);
   }
@@ -266,18 +273,16 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   };
   static_assert(sizeof(PassArgs<C>) <= 32764, "kernel parameter block too large");
   if constexpr (sizeof(C) == 8) {
-    if (a.h.tc_count > 0 && !a.h.mma_phases) {
-      // two CTAs per SM (TMEM 2 x 256 columns): keep each under ~113 KB
-      if (a.h.stages == 0) a.h.stages = 3;
-      while (a.h.stages > 2 && tc_pass_smem_bytes(a.h) > size_t(113) * 1024) --a.h.stages;
-      const size_t smem_tc = tc_pass_smem_bytes(a.h);
-      int per_sm = 0;
-      SVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_pass, kTcThreads, smem_tc));
-      if (per_sm < 1) return fail(SVB_EUNSUPPORTED, "tensor-core pass does not fit on an SM");
-      long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count * std::min(per_sm, 2));
+    if (a.h.gemm) {
+      if (a.h.tma_rank < 1) return fail(SVB_EUNSUPPORTED, "k_gemm_pass needs a tensor map");
+      const int ng = a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
+      void (*gfn)(float2*, PassArgs<float2>) = ng == 2 ? k_gemm_pass<2> : ng == 3 ? k_gemm_pass<3> : k_gemm_pass<4>;
+      const size_t smem_g = gemm_smem_layout(a.h, ng).total;
+      if (smem_g > size_t(f->max_smem)) return fail(SVB_EUNSUPPORTED, "gemm pass exceeds shared memory");
+      long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count);
       if (grid < 1) grid = 1;
-      k_tc_pass<<<(unsigned)grid, kTcThreads, smem_tc, stream>>>(reinterpret_cast<float2*>(amps),
-                                                                  reinterpret_cast<const PassArgs<float2>&>(a));
+      gfn<<<(unsigned)grid, ng * 128, smem_g, stream>>>(reinterpret_cast<float2*>(amps),
+                                                       reinterpret_cast<const PassArgs<float2>&>(a));
       SVB_CUDA(cudaGetLastError());
       return SVB_OK;
     }
@@ -347,19 +352,6 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   (void)n_local;
   return SVB_OK;
 }
-
-// TF32 round-to-nearest (ties away), as cvt.rna.tf32.f32
-float tf32_rna(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  u = (u + 0x1000u) & ~0x1FFFu;
-  float y;
-  std::memcpy(&y, &u, 4);
-  return y;
-}
-
-// K-major SWIZZLE_NONE core-matrix offset (floats) of element (n, k) of a 32x32 block
-inline int tc_bofs(int n, int k) { return ((n / 8) * 8 * 128 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) / 4; }
 
 // mma.sync m16n8k16 B fragments of the real block form of a 32x32 complex
 // phase matrix U (v_out = U v_in): B[2i + a][2j + b] with
@@ -431,7 +423,7 @@ void pack_tc(svb_plan* p) {
   for (size_t i = 0; i < p->plan.passes.size(); ++i) {
     const Pass& ps = p->plan.passes[i];
     p->tc_offset[i] = p->tc_host.size();
-    if (ps.mma_phases) {
+    if (ps.mma_phases || ps.gemm) {
       for (const auto& U : ps.tc_mats) {
         if (ps.thread_bits == 7)
           pack_t5(U, p->tc_host);
@@ -439,21 +431,6 @@ void pack_tc(svb_plan* p) {
           pack_mma(U, p->tc_host);
       }
       continue;
-    }
-    if (!ps.tensor_cores) continue;
-    for (const auto& U : ps.tc_mats) {
-      std::vector<float> blk(kTcMatBytes / 4, 0.f);
-      for (int n = 0; n < 32; ++n)
-        for (int k = 0; k < 32; ++k) {
-          const cd u = U[size_t(n) * 32 + k];
-          const float re = float(u.real()), im = float(u.imag());
-          const float rh = tf32_rna(re), ih = tf32_rna(im);
-          blk[0 * 1024 + tc_bofs(n, k)] = rh;
-          blk[1 * 1024 + tc_bofs(n, k)] = ih;
-          blk[2 * 1024 + tc_bofs(n, k)] = tf32_rna(re - rh);
-          blk[3 * 1024 + tc_bofs(n, k)] = tf32_rna(im - ih);
-        }
-      p->tc_host.insert(p->tc_host.end(), blk.begin(), blk.end());
     }
   }
 }
@@ -475,6 +452,7 @@ int upload_tc(svb_plan* p) {
 
 template <class C>
 int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int first, int count, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(p->mu);
   if (int rc = upload_tc(p)) return rc;
   for (int i = first; i < first + count; ++i) {
     int rc = launch_pass<C>(args[i], p->plan.n, static_cast<C*>(amps), s);
@@ -483,7 +461,7 @@ int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int firs
   return SVB_OK;
 }
 
-template <class C>
+template <class CA, class CB = CA>
 int dot_impl(const void* a, const void* b, long long n, double* out2, cudaStream_t s) {
   DeviceFacts* f = nullptr;
   int rc = device_facts(&f);
@@ -502,7 +480,8 @@ int dot_impl(const void* a, const void* b, long long n, double* out2, cudaStream
     SVB_CUDA(cudaMallocHost(&f->red_host, sizeof(double2) * grid));
     f->red_cap = grid;
   }
-  k_dot<C><<<(unsigned)grid, threads, 0, s>>>(static_cast<const C*>(a), static_cast<const C*>(b), n, f->red_dev);
+  k_dot<CA, CB><<<(unsigned)grid, threads, 0, s>>>(static_cast<const CA*>(a), static_cast<const CB*>(b), n,
+                                                  f->red_dev);
   SVB_CUDA(cudaGetLastError());
   SVB_CUDA(cudaMemcpyAsync(f->red_host, f->red_dev, sizeof(double2) * grid, cudaMemcpyDeviceToHost, s));
   SVB_CUDA(cudaStreamSynchronize(s));
@@ -612,7 +591,10 @@ int svb_plan_pass_info(const svb_plan* plan, int pass, svb_pass_info* out) {
   out->est_cost = p.cost;
   out->reg_bits = p.reg_bits;
   out->num_phases = int(p.phases.size());
-  out->num_tc = (p.tensor_cores || p.mma_phases) ? int(p.tc_mats.size()) : 0;
+  out->num_tc = (p.mma_phases || p.gemm) ? int(p.tc_mats.size()) : 0;
+  out->kernel = p.gemm ? SVB_KERNEL_GEMM : p.mma_phases ? SVB_KERNEL_REG_TC : p.phases.empty() ? SVB_KERNEL_TILE : SVB_KERNEL_REG;
+  out->streams = p.phases.empty() ? 1 : p.streams;
+  out->bank_conflicts = p.bank_conflicts;
   return SVB_OK;
 }
 
@@ -781,6 +763,16 @@ int svb_dot(const void* a, const void* b, int n_local, int prec, double* out2, v
   const long long n = 1LL << n_local;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return prec == SVB_C64 ? dot_impl<float2>(a, b, n, out2, s) : dot_impl<double2>(a, b, n, out2, s);
+}
+
+int svb_dot_mixed(const void* a, int prec_a, const void* b, int prec_b, int n_local, double* out2, void* stream) {
+  if (!a || !b || !out2) return fail(SVB_EINVAL, "null argument");
+  if (n_local < 0 || n_local > 62 || !valid_prec(prec_a) || !valid_prec(prec_b)) return fail(SVB_EINVAL, "bad shape");
+  const long long n = 1LL << n_local;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (prec_a == SVB_C64)
+    return prec_b == SVB_C64 ? dot_impl<float2>(a, b, n, out2, s) : dot_impl<float2, double2>(a, b, n, out2, s);
+  return prec_b == SVB_C64 ? dot_impl<double2, float2>(a, b, n, out2, s) : dot_impl<double2>(a, b, n, out2, s);
 }
 
 int svb_norm2(const void* a, int n_local, int prec, double* out, void* stream) {

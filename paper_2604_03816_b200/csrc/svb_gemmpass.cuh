@@ -1,0 +1,331 @@
+// k_gemm_pass -- c64 tile pass whose every dense op runs on the tcgen05 tensor
+// cores with BOTH operands in shared memory (the production path for c64
+// passes that carry two or more dense gates).
+//
+// A pass is  load -> ops_0 -> GEMM_1 -> ops_1 -> ... -> GEMM_P -> ops_P -> store
+// over 12-qubit tiles (4096 amplitudes, 32 KB).  GEMM_p multiplies the tile,
+// viewed as 128 rows x 32 complex columns (the phase's five register qubits
+// are the columns), by the fused 32x32 phase matrix U_p in its real 64x64
+// block form; ops_p are element-wise diagonal tables (planner: diagonal gates
+// that commute past the GEMM).  Unlike the k_reg_pass tensor-core phases,
+// nothing is transposed through registers and shared memory twice:
+//
+//   * the tile lands (TMA) in the stream's 32 KB buffer; each thread reads 32
+//     amplitudes, scales them by a power of two chosen from the tile 2-norm
+//     (all ops of the pass are unitary, so |amp| * S < 2^15 for the whole
+//     pass and the values stay scaled until the store), splits them into fp16
+//     hi + lo and writes them back IN PLACE as the A operand of GEMM_1:
+//     A_hi | A_lo, 128 rows x 128 B each, K-major SWIZZLE_128B -- the layout
+//     the tensor core reads directly through a shared-memory descriptor;
+//   * one elected thread issues the 12 tcgen05.mma.kind::f16 (M 128, N 64,
+//     K 16: Ah Bh + Al Bh + Ah Bl) into the stream's 64 TMEM columns and
+//     commits to an mbarrier;
+//   * each thread reads its D row back (tcgen05.ld: 32 complex = the row),
+//     applies ops_p in registers and -- the transpose to the next phase's
+//     column qubits -- writes hi/lo straight into A of GEMM_{p+1}
+//     (one XOR per amplitude: the swizzled word address is GF(2)-linear in
+//     the tile index);
+//   * after the last GEMM the buffer is free, so the stream's next tile load
+//     is issued at once and overlaps the store of this one; the store undoes
+//     the scale and restores the tile 2-norm (fp32 tensor-core accumulation
+//     truncates: ~1e-6 norm per GEMM).
+//
+// Four tile streams (warp groups of 128 threads, one buffer each) per CTA,
+// one CTA per SM: one stream's conversions overlap another's GEMM.  The
+// planner (build_gemm_pass) orders each phase's register and row qubits so
+// the writes land conflict-free in the shared-memory banks and the final
+// stores are coalesced.
+#pragma once
+#include "svb_regpass.cuh"
+
+namespace svb {
+
+constexpr int kGemmT = 12;            // tile qubits
+constexpr int kGemmTileBytes = 32768;  // 4096 x float2
+constexpr int kGemmAWords = 4096;      // A_hi words (f16x2); A_lo follows
+
+// lowest set bit of a (compile-time, after unrolling) loop index: the Gray
+// code of i differs from that of i - 1 in this bit
+__device__ __forceinline__ int ctz_c(int x) { return __ffs(x) - 1; }
+
+struct GemmSmem {
+  size_t pool, dthr, dout, red, mats, tiles, total;
+};
+__host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng) {
+  GemmSmem l;
+  l.pool = 128;  // barriers + TMEM slot
+  l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(float2), 128);
+  l.dout = l.dthr + align_up(size_t(h.n_ops) * 128, 128);
+  l.red = l.dout + align_up(size_t(ng) * 2 * kMaxOps * sizeof(int), 128);
+  l.mats = align_up(l.red + size_t(ng) * 8 * sizeof(float), 1024);
+  l.tiles = l.mats + size_t(h.tc_count) * kMmaMatBytes;
+  l.total = l.tiles + size_t(ng) * kGemmTileBytes;
+  return l;
+}
+
+// K-major SWIZZLE_128B shared-memory descriptor (8-row x 128-B atoms, SBO 1 KB)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void t5_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n}" ::"r"(d),
+      "l"(a), "l"(b), "r"(acc), "r"(kT5Idesc)
+      : "memory");
+}
+
+// fp16 hi/lo split of a (scaled) complex amplitude, stored as the f16x2 words
+// of A_hi and A_lo (re in the low half: K index 2j, im: 2j + 1)
+__device__ __forceinline__ void gemm_split_store(uint32_t* __restrict__ A, uint32_t w, float xr, float xi) {
+  const uint32_t hh = pack_half2(xr, xi);
+  const float2 hf = unpack_half2(hh);
+  A[w] = hh;
+  A[w + kGemmAWords] = pack_half2(xr - hf.x, xi - hf.y);
+}
+
+// Word address (in A of the phase whose table is `wt`) of the element held in
+// register 0 by this thread (layout `map`): XOR over the set thread bits.
+__device__ __forceinline__ uint32_t gemm_wbase(const PhaseDesc& cur, const unsigned short* wt, int gt) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int b = 0; b < 7; ++b)
+    if ((gt >> b) & 1) w ^= wt[cur.map[5 + b]];
+  return w;
+}
+
+// Convert the 32 registers (layout `cur`) into the A operand of the next GEMM
+// (word table `wt`), visiting registers in Gray-code order: one XOR each.
+__device__ __forceinline__ void gemm_write_a(uint32_t* __restrict__ A, const float2 (&v)[32], const PhaseDesc& cur,
+                                             const unsigned short* wt, int gt) {
+  uint32_t basis[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) basis[i] = wt[cur.map[i]];
+  uint32_t w = gemm_wbase(cur, wt, gt);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    if (i) w ^= basis[ctz_c(i)];
+    const int r = i ^ (i >> 1);
+    gemm_split_store(A, w, v[r].x, v[r].y);
+  }
+}
+
+__device__ __forceinline__ void t5_ld32x2(uint32_t taddr, float2 (&v)[32]) {
+  uint32_t d[32];
+  t5_ld32(taddr, d);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
+  t5_ld32(taddr + 32, d);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[16 + q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
+}
+
+template <int NG>
+__global__ void __launch_bounds__(NG * 128, 1)
+    k_gemm_pass(float2* __restrict__ amps, const __grid_constant__ PassArgs<float2> args) {
+  constexpr int NTG = 128;
+  constexpr int T = kGemmT;
+  constexpr uint32_t kTmemCols = NG > 2 ? 256 : 128;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const PassHeader& h = args.h;
+  const GemmSmem lay = gemm_smem_layout(h, NG);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [group] tile landed
+  uint64_t* mbar = full + NG;                           // [group] GEMM committed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + NG);
+  float2* pool = reinterpret_cast<float2*>(smem + lay.pool);
+  unsigned char* dthr = smem + lay.dthr;                 // [op][thread] diagonal index, thread part
+  int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [group][2][op] outside-tile part
+  float* red = reinterpret_cast<float*>(smem + lay.red);  // [group][in 4 | out 4] norm partials
+  const uint32_t mats = smem_addr(smem + lay.mats);
+  unsigned char* tiles = smem + lay.tiles;
+  const int tid = threadIdx.x;
+  const int group = tid / NTG, gt = tid % NTG, wig = gt >> 5, lane = tid & 31;
+  const int P = h.n_phases - 1;  // GEMM phases
+
+  if (tid == 0) {
+    for (int g = 0; g < NG; ++g) {
+      mbar_init(&full[g], 1);
+      mbar_init(&mbar[g], 1);
+    }
+    fence_mbar_init();
+  }
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tslot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int e = tid; e < h.coeff_count; e += NG * NTG) pool[e] = args.coeff[e];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(h.tc_mats);
+    uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);
+    for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += NG * NTG) dst[e] = src[e];
+  }
+  for (int e = tid; e < h.n_ops * NTG; e += NG * NTG) {
+    const OpDesc& op = args.ops[e / NTG];
+    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
+  }
+  fence_proxy_async_smem();  // B operands written by the generic proxy, read by the tensor core
+  t5_fence_before();
+  __syncthreads();
+  t5_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t dcol = tbase + uint32_t(group) * 64u + (uint32_t(wig * 32) << 16);  // this warp's D lanes
+
+  const int n_tiles = int(h.n_tiles);
+  const int mine = int(blockIdx.x) < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
+  float2* buf = reinterpret_cast<float2*>(tiles + size_t(group) * kGemmTileBytes);
+  uint32_t* A = reinterpret_cast<uint32_t*>(buf);
+  const uint32_t abase = smem_addr(buf);
+
+  // the stream's tile load (warp 0 of the group: lane 0 issues the TMA, all
+  // lanes publish the outside-tile diagonal index parts of the tile)
+  auto load = [&](int it, int xs) {
+    const int tile = int(blockIdx.x) + it * int(gridDim.x);
+    const long long tb = tile_base(tile, h);
+    if (h.has_outside) {
+      int* slot = dout + (group * 2 + xs) * kMaxOps;
+      for (int i = lane; i < h.n_ops; i += 32)
+        slot[i] = args.ops[i].kind == OP_DIAG ? diag_outside_part(args.ops[i], tb) : 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&full[group], uint32_t(kGemmTileBytes));
+      const int ne = h.n_enum;
+      const int sub = T - ne;
+      for (int e = 0; e < (1 << ne); ++e) {
+        long long origin = tb;
+        for (int j = 0; j < ne; ++j)
+          if ((e >> j) & 1) origin += 1LL << h.high[h.m - ne + j];
+        int c[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d)
+          c[d] = (d < h.tma_rank && h.tma_box[d] == 0) ? int((origin >> h.tma_start[d]) & ((1LL << h.tma_bits[d]) - 1)) : 0;
+        tma_load(buf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[group]);
+      }
+    }
+    __syncwarp();
+  };
+
+  uint32_t fpar = 0, mpar = 0;
+  int xs = 0;
+  if (wig == 0 && group < mine) load(group, 0);
+  for (int it = group; it < mine; it += NG, xs ^= 1) {
+    const int tile = int(blockIdx.x) + it * int(gridDim.x);
+    const long long origin = tile_base(tile, h);
+    const int* dslot = dout + (group * 2 + xs) * kMaxOps;
+    mbar_wait(&full[group], fpar);
+    fpar ^= 1;
+
+    // ---- phase 0: linear tile -> registers (load layout), ops_0, tile norm
+    float2 v[32];
+    {
+      const PhaseDesc& p0 = args.phases[0];
+      uint32_t x = 0, basis[5];
+#pragma unroll
+      for (int b = 0; b < 7; ++b) x |= uint32_t((gt >> b) & 1) << p0.map[5 + b];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) basis[i] = 1u << p0.map[i];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i) x ^= basis[ctz_c(i)];
+        v[i ^ (i >> 1)] = buf[x];
+      }
+      for (int o = p0.op_begin; o < p0.op_end; ++o)
+        reg_diag<float2, 5>(v, args.ops[o], pool + args.ops[o].coeff_off,
+                            int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0));
+    }
+    {
+      const float w = warp_norm2(v);
+      if (lane == 0) red[group * 8 + wig] = w;
+    }
+    group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
+    const float n2in = red[group * 8] + red[group * 8 + 1] + red[group * 8 + 2] + red[group * 8 + 3];
+    // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
+    const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
+    const int se = min(max(268 - ebits, 1), 253);
+    const float S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      v[r].x *= S;
+      v[r].y *= S;
+    }
+    gemm_write_a(A, v, args.phases[0], reinterpret_cast<const unsigned short*>(args.phases[1].R), gt);
+    fence_proxy_async_smem();
+    t5_fence_before();
+    group_bar<NG, NTG>(group);
+
+    for (int p = 1; p <= P; ++p) {
+      const PhaseDesc& ph = args.phases[p];
+      if (gt == 0) {
+        t5_fence_after();
+        const uint32_t b0 = mats + uint32_t(ph.tc) * kMmaMatBytes;
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t ad = sw128_desc(abase + (t == 1 ? uint32_t(kGemmAWords * 4) : 0u) + 32u * ks);
+            const uint64_t bd = t5_desc(b0 + (t == 2 ? 8192u : 0u) + 256u * ks, 128, 1024);
+            t5_mma_ss(tbase + uint32_t(group) * 64u, ad, bd, (t | ks) ? 1u : 0u);
+          }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_addr(&mbar[group]))
+                     : "memory");
+      }
+      mbar_wait_bounded(&mbar[group], mpar);
+      mpar ^= 1;
+      t5_fence_after();
+      // after the last GEMM the buffer is free: the next tile of this stream
+      // loads while this one is stored
+      if (p == P && wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
+      t5_ld32x2(dcol, v);
+      for (int o = ph.op_begin; o < ph.op_end; ++o)
+        reg_diag<float2, 5>(v, args.ops[o], pool + args.ops[o].coeff_off,
+                            int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0));
+      if (p < P) {
+        gemm_write_a(A, v, ph, reinterpret_cast<const unsigned short*>(args.phases[p + 1].R), gt);
+        fence_proxy_async_smem();
+        t5_fence_before();
+        group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
+        continue;
+      }
+      // ---- store: undo the scale, restore the tile 2-norm
+      t5_fence_before();
+      {
+        const float w = warp_norm2(v);
+        if (lane == 0) red[group * 8 + 4 + wig] = w;
+      }
+      group_bar<NG, NTG>(group);
+      const float n2out = red[group * 8 + 4] + red[group * 8 + 5] + red[group * 8 + 6] + red[group * 8 + 7];
+      const float f = n2out > 0.f ? sqrtf(n2in * S * S / n2out) / S : 1.f / S;
+      long long g = 0;
+      long long goff[5];
+#pragma unroll
+      for (int b = 0; b < 7; ++b)
+        if ((gt >> b) & 1) g += 1LL << gpos(ph.map[5 + b], h);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) goff[i] = 1LL << gpos(ph.map[i], h);
+      float2* __restrict__ dst = amps + origin + g;
+      long long o = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i) {
+          const int b = ctz_c(i);
+          o += ((i ^ (i >> 1)) >> b) & 1 ? goff[b] : -goff[b];
+        }
+        const int r = i ^ (i >> 1);
+        dst[o] = make_float2(v[r].x * f, v[r].y * f);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    t5_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmemCols) : "memory");
+  }
+}
+
+}  // namespace svb

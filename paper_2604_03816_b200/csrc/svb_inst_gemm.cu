@@ -1,0 +1,8 @@
+// Explicit instantiations (see svb_instances.h).
+#include "svb_gemmpass.cuh"
+
+namespace svb {
+template __global__ void k_gemm_pass<2>(float2*, const __grid_constant__ PassArgs<float2>);
+template __global__ void k_gemm_pass<3>(float2*, const __grid_constant__ PassArgs<float2>);
+template __global__ void k_gemm_pass<4>(float2*, const __grid_constant__ PassArgs<float2>);
+}  // namespace svb

@@ -378,11 +378,14 @@ __global__ void k_set_one(C* amps, long long one) {
   amps[one] = v;
 }
 
-template <class C>
-__global__ void k_dot(const C* __restrict__ a, const C* __restrict__ b, long long n, double2* __restrict__ partial) {
+// <a|b> partial sums in FP64; a and b may differ in precision (both are
+// promoted to complex128 first, as ref engines.py:340-346 promotes states)
+template <class CA, class CB = CA>
+__global__ void k_dot(const CA* __restrict__ a, const CB* __restrict__ b, long long n, double2* __restrict__ partial) {
   double re = 0.0, im = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const C x = a[i], y = b[i];
+    const CA x = a[i];
+    const CB y = b[i];
     const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
     re += xr * yr + xi * yi;  // conj(x) * y
     im += xr * yi - xi * yr;

@@ -60,18 +60,13 @@ struct PhaseDesc {
   unsigned char map[16];
 };
 
-// k_tc_pass: fused phase matrices as TF32 hi/lo pairs in the K-major
-// SWIZZLE_NONE core-matrix layout (8 rows x 16 B core matrices, LBO 128 B,
-// SBO 1024 B): [Ur_hi | Ui_hi | Ur_lo | Ui_lo], 32 x 32 fp32 each.
-constexpr int kTcMatBytes = 4 * 32 * 32 * 4;
-constexpr int kMaxTcPerPassDev = 2;
-
 // k_reg_pass mma.sync phases (c64, RB 5): the fused 32x32 complex phase
 // matrix as the real 64x64 block form B[k][n] (k = 2i + re/im of the input,
 // n = 2j + re/im of the output), split B = Bh + Bl in fp16 and stored in
 // m16n8k16 B-fragment order: [nt 0..7][kk 0..3][lane 0..31] x {bh0, bh1, bl0, bl1}.
 constexpr int kMmaMatBytes = 8 * 4 * 32 * 16;
 constexpr int kMaxMmaPerPass = 5;  // 5 x 16 KB + 4 tile streams x 32 KB fit 227 KB
+constexpr int kGemmTileBits = 12;  // k_gemm_pass tiles: 4096 amplitudes (32 KB c64)
 
 struct PassHeader {
   int T, L, m, n_ops;
@@ -92,15 +87,16 @@ struct PassHeader {
   // the non-tile bits in runs: origin = sum ((tile >> src) & (2^len-1)) << dst
   int n_gap_runs;
   int gap_src[kMaxHigh + 1], gap_dst[kMaxHigh + 1], gap_len[kMaxHigh + 1];
-  int tc_count;                 // fused GEMM matrices of this pass (k_tc_pass, or
-                                // k_reg_pass mma.sync phases when mma_phases)
+  int tc_count;                 // fused GEMM matrices of this pass (k_gemm_pass, or
+                                // k_reg_pass tensor-core phases when mma_phases)
   int has_outside;              // some diagonal op reads shard bits outside the tile
-  const float* tc_mats;         // device: tc_count * kTcMatBytes / kMmaMatBytes (set at launch)
+  const float* tc_mats;         // device: tc_count * kMmaMatBytes (set at launch)
   int mma_phases;               // k_reg_pass: tc_mats are mma.sync B fragments
   int renorm;                   // k_reg_pass (c64 RB 5): every op is unitary -- restore
                                 // each tile's 2-norm at the end of the pass
   int thread_bits;              // k_reg_pass: 8 (one tile stream) or 7 (warp groups of 128)
   int streams;                  // k_reg_pass with 7 thread bits: 2 or 3 tile streams
+  int gemm;                     // k_gemm_pass (PhaseDesc::R holds the A word table)
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)

@@ -409,9 +409,18 @@ class ShardedState:
         self.schedule = sched
         self.num_qubits = sched.n
 
+    def _reduce_device(self):
+        """Device of the reduction tensors: the shard's own GPU under NCCL (an
+        NCCL-only group has no CPU backend), host memory otherwise."""
+        import torch
+        if self.engine.dist.get_backend(self.engine.group) == "nccl":
+            return self.engine.backend.tensor(self.state).device
+        return torch.device("cpu")
+
     def norm_squared(self) -> float:
         import torch
-        v = torch.tensor([self.engine.backend.norm2(self.state)], dtype=torch.float64)
+        v = torch.tensor([self.engine.backend.norm2(self.state)], dtype=torch.float64,
+                         device=self._reduce_device())
         self.engine.dist.all_reduce(v, group=self.engine.group)
         return float(v.item())
 

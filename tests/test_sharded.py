@@ -120,3 +120,49 @@ def test_gloo_ranks_match_oracle(world, name, prec):
     assert err <= tol, err
     assert abs(norm - 1) <= (1e-10 if prec == "double" else 1e-5)
     assert swaps >= 1
+
+
+def test_norm_reduction_tensor_lives_on_the_shard_device_under_nccl():
+    """An NCCL-only process group has no CPU backend: ShardedState.norm_squared
+    must all-reduce a tensor on the shard's device (a CPU tensor
+    raised 'No backend type associated with device type cpu')."""
+    from paper_2604_03816_b200.sharded import ShardedState
+
+    seen = {}
+
+    class FakeDist:
+        def __init__(self, backend):
+            self.backend = backend
+
+        def get_backend(self, group=None):
+            return self.backend
+
+        def all_reduce(self, t, group=None):
+            seen["device"] = t.device
+            if self.backend == "nccl" and t.device.type == "cpu":
+                raise RuntimeError("No backend type associated with device type cpu")
+
+    class FakeBackend:
+        def __init__(self, dev):
+            self.t = torch.zeros(4, device=dev)
+
+        def norm2(self, state):
+            return 1.0
+
+        def tensor(self, state):
+            return self.t
+
+    class FakeEngine:
+        group = None
+
+    for backend, dev in (("nccl", "meta"), ("gloo", "cpu")):
+        eng = FakeEngine()
+        eng.dist = FakeDist(backend)
+        eng.backend = FakeBackend(dev)
+        st = ShardedState.__new__(ShardedState)
+        st.engine, st.state = eng, None
+        try:
+            st.norm_squared()
+        except (NotImplementedError, RuntimeError) as e:  # .item() on a meta tensor
+            assert "No backend type" not in str(e)
+        assert seen["device"].type == ("meta" if backend == "nccl" else "cpu")
