@@ -570,63 +570,140 @@ int gf2_rank(std::vector<int> v) {
   return r;
 }
 
-// log2 of the bank-conflict degree when the lanes of layout `cur` (tile bits
-// cur[5..9]) store 4-byte words into the A operand laid out by `nxt`
+// Shared-memory wavefronts of one warp instruction: lanes l = 0..31 access
+// `bytes` at byte address addr[l]; the warp is served in groups of 128 / bytes
+// lanes, each group in as many wavefronts as its most-loaded bank has
+// distinct 4-byte words.  Returns log2(wavefronts / ideal).
+int smem_excess(const std::vector<long long>& addr, int bytes) {
+  const int per = 128 / bytes;
+  int total = 0;
+  for (int g0 = 0; g0 < 32; g0 += per) {
+    std::vector<std::vector<long long>> bank(32);
+    for (int l = g0; l < g0 + per; ++l)
+      for (int w = 0; w < bytes / 4; ++w) {
+        const long long word = addr[l] / 4 + w;
+        auto& v = bank[word % 32];
+        if (std::find(v.begin(), v.end(), word) == v.end()) v.push_back(word);
+      }
+    int mx = 0;
+    for (auto& v : bank) mx = std::max(mx, int(v.size()));
+    total += mx;
+  }
+  const int ideal = 32 * bytes / 128;
+  int lg = 0;
+  while ((ideal << lg) < total) ++lg;
+  return lg;
+}
+
+// tile index of the element in register `rho` of lane `lane` (warp 0) of a thread layout
+long long lane_elem(const int* map, int lane, int rho) {
+  long long x = 0;
+  for (int i = 0; i < 5; ++i)
+    if ((rho >> i) & 1) x |= 1LL << map[i];
+  for (int b = 0; b < 5; ++b)
+    if ((lane >> b) & 1) x |= 1LL << map[5 + b];
+  return x;
+}
+
+// A writes (STS.32 of f16x2 words) from thread layout `cur` into the A layout `nxt`
 int gemm_write_conflict(const int* cur, const int* nxt) {
   unsigned short wt[16];
   gemm_word_table(nxt, wt);
-  std::vector<int> v;
-  for (int b = 0; b < 5; ++b) v.push_back(wt[cur[5 + b]] & 31);
-  return 5 - gf2_rank(v);
+  std::vector<long long> addr(32);
+  for (int l = 0; l < 32; ++l) {
+    const long long x = lane_elem(cur, l, 0);
+    int w = 0;
+    for (int t = 0; t < kGemmTileBits; ++t)
+      if ((x >> t) & 1) w ^= wt[t];
+    addr[l] = 4LL * w;
+  }
+  return smem_excess(addr, 4);
 }
 
-// log2 of the extra 128-B segments of 8-byte accesses whose lanes are tile
-// bits lanes[0..4] of the linear tile (coalesced loads / stores need the four
-// lowest tile bits -- 16 amplitudes = 128 B -- on the lanes)
-int linear_lane_cost(const int* lanes) {
-  std::vector<int> v;
-  for (int b = 0; b < 5; ++b) v.push_back(lanes[b] < 4 ? (1 << lanes[b]) : 0);
-  return 4 - gf2_rank(v);
+// Loads of the linear TMA tile in the load layout (16-byte pairs when register
+// bit 0 is tile bit 0, else 8-byte amplitudes)
+int gemm_load_conflict(const int* map0) {
+  const int bytes = map0[0] == 0 ? 16 : 8;
+  std::vector<long long> addr(32);
+  for (int l = 0; l < 32; ++l) addr[l] = 8 * lane_elem(map0, l, 0);
+  return smem_excess(addr, bytes);
 }
 
-// Layout of GEMM phase f given the lanes of the previous layout: the previous
-// lanes that are register bits of f go to j0, j1 (bank bits 0, 1) and then to
-// j2..j4, those that are row bits to m0..m2 (bank bits 2..4 -- XOR-paired
-// with j2..j4, so a pair never shares a bank bit); the other lane positions
-// take row bits the next boundary wants (`pref`, in order).
-void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pref, int* map) {
+// log2 of the extra 128-B segments of the final global stores (tile bits
+// below L are contiguous; anything above lands in another segment)
+int gemm_store_cost(const int* map, int L) {
+  const int bytes = map[0] == 0 ? 16 : 8;
+  std::vector<long long> seg;
+  for (int l = 0; l < 32; ++l) {
+    const long long x = lane_elem(map, l, 0);
+    const long long lo = x & ((1LL << L) - 1), hi = x >> L;
+    const long long key = (hi << 40) | ((8 * lo) / 128);
+    if (std::find(seg.begin(), seg.end(), key) == seg.end()) seg.push_back(key);
+  }
+  const int ideal = 32 * bytes / 128;
+  int lg = 0;
+  while ((ideal << lg) < int(seg.size())) ++lg;
+  return lg;
+}
+
+// Thread layout of a GEMM phase's D read-out: 32x32b -> thread = row (m0..m6),
+// registers = columns j0..j4; 16x256b -> registers j2 j3 j4 m3 m4, lanes
+// j0 j1 m0 m1 m2, warps m5 m6 (see gemm_read_half)
+void gemm_thread_map(const int* alay, bool ld16, int* map) {
+  if (!ld16) {
+    for (int i = 0; i < 12; ++i) map[i] = alay[i];
+    return;
+  }
+  const int m[12] = {alay[2], alay[3], alay[4], alay[5 + 3], alay[5 + 4],
+                     alay[0], alay[1], alay[5 + 0], alay[5 + 1], alay[5 + 2], alay[5 + 5], alay[5 + 6]};
+  for (int i = 0; i < 12; ++i) map[i] = m[i];
+}
+
+// A layout of GEMM phase f (j0..j4 = register qubits, m0..m6 = rows) given the
+// lanes of the writing layout: previous lanes that are register qubits go to
+// j0, j1 (bank bits 0, 1) and then to j2..j4, those that are row qubits to
+// m0..m2 (bank bits 2..4 -- XOR-paired with j2..j4, so a pair never shares a
+// bank bit).  `j01` (optional) claims j0, j1 first (low qubits on the lanes of
+// a 16x256b read-out); the free lane rows take the qubits in `pref`.
+void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pref, const std::vector<int>* j01,
+                 int* alay) {
   const int T = kGemmTileBits;
   std::vector<int> inR(T, 0);
   for (int i = 0; i < 5; ++i) inR[R[i]] = 1;
   std::vector<int> X, Y;
   for (int b = 0; b < 5; ++b) (inR[prev_lanes[b]] ? X : Y).push_back(prev_lanes[b]);
   int j[5] = {-1, -1, -1, -1, -1}, m[7] = {-1, -1, -1, -1, -1, -1, -1};
-  bool slot_used[3] = {false, false, false};  // bank bits 2..4
-  size_t xi = 0;
-  for (int s = 0; s < 2 && xi < X.size(); ++s) j[s] = X[xi++];
-  for (size_t yi = 0; yi < Y.size() && yi < 3; ++yi) {
-    m[yi] = Y[yi];
-    slot_used[yi] = true;
-  }
-  for (int s = 0; s < 3 && xi < X.size(); ++s)
-    if (!slot_used[s]) {
-      j[2 + s] = X[xi++];
-      slot_used[s] = true;
-    }
   std::vector<int> used(T, 0);
-  for (int i = 0; i < 5; ++i)
-    if (j[i] >= 0) used[j[i]] = 1;
-  for (int i = 0; i < 7; ++i)
-    if (m[i] >= 0) used[m[i]] = 1;
-  // leftovers of the previous lanes (conflicting) first, then the rest
-  for (int i = 0; i < 5; ++i)
-    if (j[i] < 0)
-      for (int t : X)
-        if (!used[t]) {
-          j[i] = t;
-          used[t] = 1;
-          break;
-        }
+  int s = 0;
+  if (j01)
+    for (int t : *j01)
+      if (s < 2 && inR[t] && !used[t]) {
+        j[s++] = t;
+        used[t] = 1;
+      }
+  for (int t : X)
+    if (s < 2 && !used[t]) {
+      j[s++] = t;
+      used[t] = 1;
+    }
+  bool slot_used[3] = {false, false, false};  // bank bits 2..4
+  int yi = 0;
+  for (int t : Y)
+    if (yi < 3) {
+      m[yi] = t;
+      used[t] = 1;
+      slot_used[yi++] = true;
+    }
+  for (int t : X) {
+    if (used[t]) continue;
+    for (int sl = 0; sl < 3; ++sl)
+      if (!slot_used[sl] && j[2 + sl] < 0) {
+        j[2 + sl] = t;
+        used[t] = 1;
+        slot_used[sl] = true;
+        break;
+      }
+  }
   for (int i = 0; i < 5; ++i)
     if (j[i] < 0)
       for (int q = 0; q < 5; ++q)
@@ -635,13 +712,14 @@ void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pr
           used[R[q]] = 1;
           break;
         }
-  for (size_t yi = 3; yi < Y.size(); ++yi)
-    for (int i = 0; i < 7; ++i)
-      if (m[i] < 0) {
-        m[i] = Y[yi];
-        used[Y[yi]] = 1;
-        break;
-      }
+  for (int t : Y)
+    if (!used[t])
+      for (int i = 0; i < 7; ++i)
+        if (m[i] < 0) {
+          m[i] = t;
+          used[t] = 1;
+          break;
+        }
   for (int i = 0; i < 7; ++i) {
     if (m[i] >= 0) continue;
     int pick = -1;
@@ -660,8 +738,8 @@ void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pr
     m[i] = pick;
     used[pick] = 1;
   }
-  for (int i = 0; i < 5; ++i) map[i] = j[i];
-  for (int b = 0; b < 7; ++b) map[5 + b] = m[b];
+  for (int i = 0; i < 5; ++i) alay[i] = j[i];
+  for (int b = 0; b < 7; ++b) alay[5 + b] = m[b];
 }
 
 // Lower a pass (12-qubit tile, unitary ops) for k_gemm_pass: list-schedule
@@ -670,7 +748,7 @@ void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pr
 // bits before or after the GEMM they commute with, and choose every phase's
 // qubit order for conflict-free A writes and coalesced loads / stores.
 // Returns false (pass left unchanged) when the pass does not fit the kernel.
-bool build_gemm_pass(Pass& p) {
+bool build_gemm_pass(Pass& p, int streams) {
   const int T = kGemmTileBits;
   if (p.T != T) return false;
   for (const KernelOp& op : p.ops) {  // unitary ops only (the kernel rescales by the tile norm)
@@ -720,28 +798,42 @@ bool build_gemm_pass(Pass& p) {
       for (int i = ph.op_begin; i < ph.op_end; ++i) (gps.empty() ? pre0 : gps.back().post).push_back(i);
       continue;
     }
-    GP g;
-    for (int i = 0; i < 5; ++i) g.R[i] = R[i];
-    g.U.assign(size_t(D) * D, cd());
-    for (int r = 0; r < D; ++r) g.U[size_t(r) * D + r] = 1.0;
+    // segments: ops fold into the open GEMM; a diagonal op on row / outside
+    // qubits moves after it (commutes with the phase's later dense ops) or
+    // before it (commutes with the dense ops folded so far), else the GEMM is
+    // closed there and the op runs between it and the next one (same columns)
+    auto fresh = [&]() {
+      GP g;
+      for (int i = 0; i < 5; ++i) g.R[i] = R[i];
+      g.U.assign(size_t(D) * D, cd());
+      for (int r = 0; r < D; ++r) g.U[size_t(r) * D + r] = 1.0;
+      return g;
+    };
+    GP g = fresh();
+    unsigned long long folded = 0;  // dense qubits folded into the open GEMM
     std::vector<int> pre;
     for (int i = ph.op_begin; i < ph.op_end; ++i) {
       const KernelOp& op = q.ops[i];
       const unsigned long long b = bits_of(op);
       const bool reg_only = (b & ~(unsigned long long)rmask) == 0;
       if (op.kind == OP_DIAG && !reg_only) {
-        unsigned long long before = 0, after = 0;
-        for (int k = ph.op_begin; k < ph.op_end; ++k)
-          (k < i ? before : after) |= k == i ? 0ULL : dense_bits[k - ph.op_begin];
+        unsigned long long after = 0;
+        for (int k = i + 1; k < ph.op_end; ++k) after |= dense_bits[k - ph.op_begin];
         if ((b & after) == 0) {
           g.post.push_back(i);
-        } else if ((b & before) == 0) {
+        } else if ((b & folded) == 0) {
           pre.push_back(i);
         } else {
-          return false;
+          for (int k : pre) (gps.empty() ? pre0 : gps.back().post).push_back(k);
+          pre.clear();
+          g.post.push_back(i);
+          gps.push_back(std::move(g));
+          g = fresh();
+          folded = 0;
         }
         continue;
       }
+      if (op.kind == OP_DENSE) folded |= b;
       // fold into U: M (in ascending-R index space) times U
       int pos[kMaxK];
       for (int j = 0; j < op.k; ++j) pos[j] = rpos(op.tgt[j]);
@@ -775,49 +867,58 @@ bool build_gemm_pass(Pass& p) {
   const int P = int(gps.size());
   if (P < 1 || P > kMaxMmaPerPass || P + 1 > kMaxPhases) return false;
 
-  // ---- layouts: choose the load lanes, then each GEMM phase greedily
-  std::vector<std::vector<int>> maps(P + 1, std::vector<int>(16, 0));
-  auto pref_for = [&](int f) {  // row bits phase f's lanes should carry
+  // ---- layouts.  Load lanes: tile qubits 1, 2, 3 (conflict-free 16-byte
+  // loads with tile qubit 0 in register bit 0) plus two more; then each GEMM
+  // phase greedily (A layout from the writing lanes) with a 32x32b or 16x256b
+  // D read-out.  Cost: smem wavefronts of the loads and A writes, 128-B
+  // segments of the final stores (doubled: global).
+  const std::vector<int> low = {0, 1, 2, 3};
+  auto pref_for = [&](int f) {  // qubits the lanes of GEMM phase f should carry
     std::vector<int> pr;
     if (f < P) {
       for (int i = 0; i < 5; ++i) pr.push_back(gps[f].R[i]);  // gps[f] is GEMM phase f + 1
     } else {
-      for (int t = 0; t < 4; ++t) pr.push_back(t);  // coalesced stores
+      pr = low;
     }
     return pr;
   };
   int best_cost = 1 << 30;
-  std::vector<std::vector<int>> best;
-  std::vector<int> sel(5);
+  std::vector<std::vector<int>> best_maps, best_alay;
+  std::vector<int> best_ld16;
+  const int n_shape = P <= 3 ? (1 << P) : 2;
   for (int a = 0; a < T; ++a)
-    for (int b = a + 1; b < T; ++b)
-      for (int c = b + 1; c < T; ++c)
-        for (int d = c + 1; d < T; ++d)
-          for (int e = d + 1; e < T; ++e) {
-            const int lanes[5] = {a, b, c, d, e};
-            std::vector<std::vector<int>> mp(P + 1, std::vector<int>(16, 0));
-            // load layout: lanes, then registers, then the two warp bits
-            std::vector<int> rest;
-            for (int t = 0; t < T; ++t)
-              if (t != a && t != b && t != c && t != d && t != e) rest.push_back(t);
-            for (int i = 0; i < 5; ++i) mp[0][i] = rest[i];
-            for (int i = 0; i < 5; ++i) mp[0][5 + i] = lanes[i];
-            mp[0][10] = rest[5];
-            mp[0][11] = rest[6];
-            int cost = linear_lane_cost(lanes);
-            for (int f = 1; f <= P; ++f) {
-              gemm_layout(&mp[f - 1][5], gps[f - 1].R, pref_for(f), mp[f].data());
-              cost += 2 * gemm_write_conflict(mp[f - 1].data(), mp[f].data());
-            }
-            cost += 2 * linear_lane_cost(&mp[P][5]);
-            if (cost < best_cost) {
-              best_cost = cost;
-              best = mp;
-            }
-          }
-  maps = best;
+    for (int b = a + 1; b < T; ++b) {
+      if (a <= 3 || b <= 3) continue;  // lanes = {1, 2, 3, a, b}
+      for (int shape = 0; shape < n_shape * 2; ++shape) {
+        std::vector<std::vector<int>> mp(P + 1, std::vector<int>(16, 0)), al(P + 1, std::vector<int>(16, 0));
+        std::vector<int> ld16(P + 1, 0);
+        // load layout: register bit 0 = tile qubit 0, lanes 1 2 3 a b
+        std::vector<int> rest;
+        for (int t = 0; t < T; ++t)
+          if (t != 0 && t != 1 && t != 2 && t != 3 && t != a && t != b) rest.push_back(t);
+        const int m0[12] = {0, rest[0], rest[1], rest[2], rest[3], 1, 2, 3, a, b, rest[4], rest[5]};
+        for (int i = 0; i < 12; ++i) mp[0][i] = m0[i];
+        int cost = gemm_load_conflict(mp[0].data());
+        for (int f = 1; f <= P; ++f) {
+          const bool last = f == P;
+          ld16[f] = n_shape == 2 ? (last ? (shape & 1) : 0) : ((shape >> (f - 1)) & 1);
+          const bool lowj = last && ld16[f] && (shape >> (n_shape == 2 ? 1 : P)) & 1;
+          gemm_layout(&mp[f - 1][5], gps[f - 1].R, pref_for(f), lowj ? &low : nullptr, al[f].data());
+          gemm_thread_map(al[f].data(), ld16[f], mp[f].data());
+          cost += 2 * gemm_write_conflict(mp[f - 1].data(), al[f].data());
+        }
+        cost += 3 * gemm_store_cost(mp[P].data(), p.L);
+        if (cost < best_cost) {
+          best_cost = cost;
+          best_maps = mp;
+          best_alay = al;
+          best_ld16 = ld16;
+        }
+      }
+    }
+  const std::vector<std::vector<int>>& maps = best_maps;
   int conflicts = 0;
-  for (int f = 1; f <= P; ++f) conflicts += gemm_write_conflict(maps[f - 1].data(), maps[f].data());
+  for (int f = 1; f <= P; ++f) conflicts += gemm_write_conflict(maps[f - 1].data(), best_alay[f].data());
 
   // ---- assemble: ops in execution order, phases, GEMM matrices in layout order
   std::vector<int> order;
@@ -839,7 +940,9 @@ bool build_gemm_pass(Pass& p) {
     RegPhase rp;
     const int* mp = maps[f].data();
     for (int i = 0; i < 16; ++i) rp.map[i] = i < T ? mp[i] : 0;
-    for (int i = 0; i < 5; ++i) rp.R[i] = mp[i];
+    // R = the GEMM's column qubits in matrix order (the A layout's j0..j4);
+    // the load phase has no GEMM: its register qubits
+    for (int i = 0; i < 5; ++i) rp.R[i] = f == 0 ? mp[i] : best_alay[f][i];
     rp.op_begin = ranges[f].first;
     rp.op_end = ranges[f].second;
     if (f == 0) {
@@ -848,14 +951,16 @@ bool build_gemm_pass(Pass& p) {
     } else {
       rp.op_mid = rp.op_begin;  // GEMM first, then the diagonal ops
       rp.tc = f - 1;
-      gemm_word_table(mp, rp.wt);
+      if (best_ld16[f]) rp.flags |= PH_LD16;
+      const int* al = best_alay[f].data();
+      gemm_word_table(al, rp.wt);
       rp.tc_gates = gps[f - 1].gates;
-      // U in the layout's register order: register bit i <-> tile bit mp[i]
+      // U in the A layout's column order: column bit i <-> tile bit al[i]
       const int* R = gps[f - 1].R;
       int to_asc[5];
       for (int i = 0; i < 5; ++i)
         for (int k = 0; k < 5; ++k)
-          if (R[k] == mp[i]) to_asc[i] = k;
+          if (R[k] == al[i]) to_asc[i] = k;
       auto conv = [&](int x) {
         int y = 0;
         for (int i = 0; i < 5; ++i) y |= ((x >> i) & 1) << to_asc[i];
@@ -916,7 +1021,7 @@ bool build_gemm_pass(Pass& p) {
   }
   p.reg_bits = 5;
   p.thread_bits = 7;
-  p.streams = 4;
+  p.streams = streams >= 2 && streams <= 4 ? streams : 4;
   p.gemm = true;
   p.mma_phases = false;
   p.renorm = true;
@@ -1310,7 +1415,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     int n_dense = 0;
     for (const KernelOp& o : p.ops) n_dense += o.kind == OP_DENSE;
     const int min_dense = opt.tc_min_dense > 0 ? opt.tc_min_dense : 2;
-    if (use_gemm && p.T == kGemmTileBits && n_dense >= min_dense && build_gemm_pass(p)) {
+    if (use_gemm && p.T == kGemmTileBits && n_dense >= min_dense && build_gemm_pass(p, opt.streams)) {
       // k_gemm_pass (lowered above)
     } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
       // 12-qubit tiles: warp groups with their own tile streams (k_reg_pass TB 7)

@@ -44,9 +44,13 @@ constexpr int kGemmT = 12;            // tile qubits
 constexpr int kGemmTileBytes = 32768;  // 4096 x float2
 constexpr int kGemmAWords = 4096;      // A_hi words (f16x2); A_lo follows
 
-// lowest set bit of a (compile-time, after unrolling) loop index: the Gray
-// code of i differs from that of i - 1 in this bit
-__device__ __forceinline__ int ctz_c(int x) { return __ffs(x) - 1; }
+// lowest set bit of a loop index 1..31: the Gray code of i differs from that
+// of i - 1 in this bit.  Plain selects, so that after unrolling the index of
+// every register-array access folds to a constant (a dynamic index would put
+// the array in local memory)
+__host__ __device__ __forceinline__ constexpr int ctz_c(int x) {
+  return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : 4;
+}
 
 struct GemmSmem {
   size_t pool, dthr, dout, red, mats, tiles, total;
@@ -112,15 +116,75 @@ __device__ __forceinline__ void gemm_write_a(uint32_t* __restrict__ A, const flo
   }
 }
 
-__device__ __forceinline__ void t5_ld32x2(uint32_t taddr, float2 (&v)[32]) {
+// tcgen05.ld 16x256b, 8 repetitions: 16 TMEM lanes x 64 columns per warp;
+// thread t gets rows t/4 and t/4 + 8, columns 8c + 2 (t % 4) + {0, 1}
+__device__ __forceinline__ void t5_ld16x256_x8(uint32_t taddr, uint32_t (&d)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+        "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]),
+        "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]),
+        "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+// One half (register index bit 4 = `half`) of this thread's 32 amplitudes of
+// the D tile, in the phase's thread layout:
+//  * 32x32b (thread = row m; register index = column j): columns 32 half ..;
+//  * 16x256b (PH_LD16): register index = j2 j3 j4 | row bit 3 | row bit 4 =
+//    half; lanes = j0 j1 | row bits 0..2 -- two column bits on the lanes,
+//    which lets the planner put low tile qubits there (coalesced stores,
+//    conflict-free A writes).
+__device__ __forceinline__ void gemm_read_half(uint32_t dcol, bool ld16, int half, float2 (&u)[16]) {
   uint32_t d[32];
-  t5_ld32(taddr, d);
+  if (!ld16) {
+    t5_ld32(dcol + 32u * half, d);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int q = 0; q < 16; ++q) v[q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
-  t5_ld32(taddr + 32, d);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int q = 0; q < 16; ++q) u[q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
+  } else {
+    t5_ld16x256_x8(dcol + (uint32_t(16 * half) << 16), d);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int q = 0; q < 16; ++q) v[16 + q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        u[c | hh << 3] = make_float2(__uint_as_float(d[4 * c + 2 * hh]), __uint_as_float(d[4 * c + 2 * hh + 1]));
+  }
+}
+
+// Diagonal op on one half: one table factor per amplitude (table index =
+// thread part | register part rmap[rho] | outside-tile part); no hoisted
+// factors, so register pressure stays at the 16 amplitudes.
+__device__ __forceinline__ void gemm_diag_half(float2 (&u)[16], const OpDesc& op, const float2* __restrict__ table,
+                                               int dbase, int half) {
+  const unsigned char* rmap = reinterpret_cast<const unsigned char*>(op.tgt);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) u[q] = cmul(u[q], table[dbase | rmap[q | half << 4]]);
+}
+
+// Convert one half into the A operand of the next GEMM (word table `wt`).
+__device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const float2 (&u)[16], const PhaseDesc& cur,
+                                                const unsigned short* wt, int gt, int half) {
+  uint32_t basis[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) basis[i] = wt[cur.map[i]];
+  uint32_t w = gemm_wbase(cur, wt, gt) ^ (half ? uint32_t(wt[cur.map[4]]) : 0u);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i) w ^= basis[ctz_c(i)];
+    const int r = i ^ (i >> 1);
+    gemm_split_store(A, w, u[r].x, u[r].y);
+  }
+}
+
+__device__ __forceinline__ float norm2_16(const float2 (&u)[16]) {
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) s = fmaf(u[q].x, u[q].x, fmaf(u[q].y, u[q].y, s));
+  return s;
 }
 
 template <int NG>
@@ -221,45 +285,64 @@ __global__ void __launch_bounds__(NG * 128, 1)
     fpar ^= 1;
 
     // ---- phase 0: linear tile -> registers (load layout), ops_0, tile norm
-    float2 v[32];
+    float S, n2in;
     {
+      float2 v[32];
       const PhaseDesc& p0 = args.phases[0];
-      uint32_t x = 0, basis[5];
+      uint32_t x = 0;
 #pragma unroll
       for (int b = 0; b < 7; ++b) x |= uint32_t((gt >> b) & 1) << p0.map[5 + b];
+      if (p0.map[0] == 0) {
+        // register bit 0 = tile bit 0: adjacent pairs, 16-byte loads
+        uint32_t basis[4];
 #pragma unroll
-      for (int i = 0; i < 5; ++i) basis[i] = 1u << p0.map[i];
+        for (int i = 0; i < 4; ++i) basis[i] = 1u << p0.map[1 + i];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (i) x ^= basis[ctz_c(i)];
-        v[i ^ (i >> 1)] = buf[x];
+        for (int i = 0; i < 16; ++i) {
+          if (i) x ^= basis[ctz_c(i)];
+          const float4 q = *reinterpret_cast<const float4*>(buf + x);
+          const int r = (i ^ (i >> 1)) << 1;
+          v[r] = make_float2(q.x, q.y);
+          v[r | 1] = make_float2(q.z, q.w);
+        }
+      } else {
+        uint32_t basis[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) basis[i] = 1u << p0.map[i];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i) x ^= basis[ctz_c(i)];
+          v[i ^ (i >> 1)] = buf[x];
+        }
       }
-      for (int o = p0.op_begin; o < p0.op_end; ++o)
-        reg_diag<float2, 5>(v, args.ops[o], pool + args.ops[o].coeff_off,
-                            int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0));
-    }
-    {
-      const float w = warp_norm2(v);
-      if (lane == 0) red[group * 8 + wig] = w;
-    }
-    group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
-    const float n2in = red[group * 8] + red[group * 8 + 1] + red[group * 8 + 2] + red[group * 8 + 3];
-    // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
-    const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
-    const int se = min(max(268 - ebits, 1), 253);
-    const float S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
+      {
+        const float w = warp_norm2(v);
+        if (lane == 0) red[group * 8 + wig] = w;
+      }
+      group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
+      n2in = red[group * 8] + red[group * 8 + 1] + red[group * 8 + 2] + red[group * 8 + 3];
+      // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
+      const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
+      const int se = min(max(268 - ebits, 1), 253);
+      S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      v[r].x *= S;
-      v[r].y *= S;
+      for (int half = 0; half < 2; ++half) {
+        float2 u[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) u[q] = make_float2(v[q | half << 4].x * S, v[q | half << 4].y * S);
+        for (int o = p0.op_begin; o < p0.op_end; ++o)
+          gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
+                         int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
+        gemm_write_half(A, u, p0, reinterpret_cast<const unsigned short*>(args.phases[1].R), gt, half);
+      }
     }
-    gemm_write_a(A, v, args.phases[0], reinterpret_cast<const unsigned short*>(args.phases[1].R), gt);
     fence_proxy_async_smem();
     t5_fence_before();
     group_bar<NG, NTG>(group);
 
     for (int p = 1; p <= P; ++p) {
       const PhaseDesc& ph = args.phases[p];
+      const bool ld16 = ph.flags & PH_LD16;
       if (gt == 0) {
         t5_fence_after();
         const uint32_t b0 = mats + uint32_t(ph.tc) * kMmaMatBytes;
@@ -278,47 +361,81 @@ __global__ void __launch_bounds__(NG * 128, 1)
       mbar_wait_bounded(&mbar[group], mpar);
       mpar ^= 1;
       t5_fence_after();
-      // after the last GEMM the buffer is free: the next tile of this stream
-      // loads while this one is stored
-      if (p == P && wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
-      t5_ld32x2(dcol, v);
-      for (int o = ph.op_begin; o < ph.op_end; ++o)
-        reg_diag<float2, 5>(v, args.ops[o], pool + args.ops[o].coeff_off,
-                            int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0));
       if (p < P) {
-        gemm_write_a(A, v, ph, reinterpret_cast<const unsigned short*>(args.phases[p + 1].R), gt);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float2 u[16];
+          gemm_read_half(dcol, ld16, half, u);
+          for (int o = ph.op_begin; o < ph.op_end; ++o)
+            gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
+                           int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
+          gemm_write_half(A, u, ph, reinterpret_cast<const unsigned short*>(args.phases[p + 1].R), gt, half);
+        }
         fence_proxy_async_smem();
         t5_fence_before();
         group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
         continue;
       }
-      // ---- store: undo the scale, restore the tile 2-norm
-      t5_fence_before();
+      // ---- last GEMM done: the buffer is free, so this stream's next tile
+      // loads while this one is stored
+      if (wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
+      // tile 2-norm of the result (diagonal ops are unimodular: applied after)
       {
-        const float w = warp_norm2(v);
+        float w = 0.f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float2 u[16];
+          gemm_read_half(dcol, ld16, half, u);
+          w += norm2_16(u);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
         if (lane == 0) red[group * 8 + 4 + wig] = w;
       }
       group_bar<NG, NTG>(group);
       const float n2out = red[group * 8 + 4] + red[group * 8 + 5] + red[group * 8 + 6] + red[group * 8 + 7];
+      // undo the scale, restore the tile 2-norm (all ops unitary)
       const float f = n2out > 0.f ? sqrtf(n2in * S * S / n2out) / S : 1.f / S;
       long long g = 0;
-      long long goff[5];
 #pragma unroll
       for (int b = 0; b < 7; ++b)
         if ((gt >> b) & 1) g += 1LL << gpos(ph.map[5 + b], h);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) goff[i] = 1LL << gpos(ph.map[i], h);
       float2* __restrict__ dst = amps + origin + g;
-      long long o = 0;
+      const bool pairs = ph.map[0] == 0;  // register bit 0 = tile bit 0: 16-byte stores
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (i) {
-          const int b = ctz_c(i);
-          o += ((i ^ (i >> 1)) >> b) & 1 ? goff[b] : -goff[b];
+      for (int half = 0; half < 2; ++half) {
+        float2 u[16];
+        gemm_read_half(dcol, ld16, half, u);
+        for (int o = ph.op_begin; o < ph.op_end; ++o)
+          gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
+                         int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
+        long long goff[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) goff[i] = 1LL << gpos(ph.map[i], h);
+        long long o = half ? goff[4] : 0;
+        if (pairs) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i) {
+              const int b = ctz_c(i) + 1;
+              o += (((i ^ (i >> 1)) << 1) >> b) & 1 ? goff[b] : -goff[b];
+            }
+            const int r = (i ^ (i >> 1)) << 1;
+            *reinterpret_cast<float4*>(dst + o) = make_float4(u[r].x * f, u[r].y * f, u[r | 1].x * f, u[r | 1].y * f);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i) {
+              const int b = ctz_c(i);
+              o += ((i ^ (i >> 1)) >> b) & 1 ? goff[b] : -goff[b];
+            }
+            const int r = i ^ (i >> 1);
+            dst[o] = make_float2(u[r].x * f, u[r].y * f);
+          }
         }
-        const int r = i ^ (i >> 1);
-        dst[o] = make_float2(v[r].x * f, v[r].y * f);
       }
+      t5_fence_before();
     }
   }
   __syncthreads();

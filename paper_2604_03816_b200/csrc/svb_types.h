@@ -47,7 +47,8 @@ struct OpDesc {
 // OpDesc.srt[0..kt) = thread bits, OpDesc.tgt viewed as 32 bytes = the
 // register part of the table index for each rho).
 constexpr int kMaxPhases = 32;
-enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2, PH_MMA = 4 };
+enum PhaseFlags : int { PH_TRANSPOSE_IN = 1, PH_TRANSPOSE_OUT = 2, PH_MMA = 4,
+                        PH_LD16 = 8 /* k_gemm_pass: D read out with tcgen05.ld 16x256b */ };
 
 struct PhaseDesc {
   int op_begin, op_end, flags, tc;  // tc >= 0: tensor-core GEMM tc between [op_begin,op_mid) and [op_mid,op_end)

@@ -179,6 +179,19 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
             for ph in phases:
                 R = ph["R"][:rb]
                 mp = ph["map"]
+                if info["kernel"] == "gemm":
+                    # k_gemm_pass: the GEMM acts on the column qubits R (matrix
+                    # order), then the diagonal ops in the read-out layout `map`
+                    if ph["tc"] >= 0:
+                        gm = list(R) + [q for q in range(T) if q not in R]
+                        base = np.zeros(nthreads, dtype=np.int64)
+                        for k in range(T - rb):
+                            base |= ((tid >> k) & 1) << gm[rb + k]
+                        cl = np.stack([base + sum(1 << gm[i] for i in range(rb) if (rho >> i) & 1)
+                                       for rho in range(nr)], axis=1)
+                        U = nat.tc_matrix(p, ph["tc"]).astype(buf.dtype)
+                        buf[cl] = buf[cl] @ U.T
+                    ph = dict(ph, tc=-1, op_mid=ph["op_begin"])
                 assert sorted(mp[:T]) == list(range(T)), mp  # the layout is a bit permutation
                 if ph["mma"] and T - rb == 8:
                     # fragment layout (svb_regpass.cuh mma_phase): K bits R[2..4] in
@@ -337,3 +350,65 @@ def test_mma_plans_layered28():
     infos = plan.passes()
     assert sum(i["num_tc"] for i in infos) > 0
     assert sum(i["num_gates"] for i in infos) == 189
+
+
+def _mixed_circuit(n: int, layers: int, seed: int) -> Circuit:
+    """Dense 2q gates on neighbours, diagonal CP / CZ-type gates on far pairs,
+    RZ and H: fused passes whose GEMMs interleave with diagonal ops on row and
+    outside-tile qubits."""
+    rng = np.random.default_rng(seed)
+    gates = []
+    for layer in range(layers):
+        for q in range(layer % 2, n - 1, 2):
+            z = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+            u, _ = np.linalg.qr(z)
+            gates.append(GateOp(GateKind.CUSTOM, (q, q + 1), (), u))
+        for _ in range(n // 2):
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            ph = np.exp(1j * rng.uniform(0, 2 * np.pi, 4))
+            gates.append(GateOp(GateKind.CUSTOM, (min(a, b), max(a, b)), (), np.diag(ph)))
+        for q in range(n):
+            gates.append(GateOp(GateKind.RZ if (q + layer) % 3 else GateKind.H, (q,),
+                                (rng.uniform(0, 6),) if (q + layer) % 3 else ()))
+    return Circuit(n, gates)
+
+
+GEMM_CASES = [
+    ("layered16", lambda: fuse(gen.layered_circuit(16, layers=8, seed=2), 2)[0]),
+    ("qft16", lambda: fuse(gen.qft_circuit(16), 2)[0]),
+    ("qft18_w3", lambda: fuse(gen.qft_circuit(18), 3)[0]),
+    ("mixed15", lambda: fuse(_mixed_circuit(15, 6, 3), 2)[0]),
+    ("mixed14_raw", lambda: _mixed_circuit(14, 4, 4)),
+]
+
+
+@pytest.mark.parametrize("name,make", GEMM_CASES, ids=[c[0] for c in GEMM_CASES])
+def test_gemm_pass_encoding(name, make):
+    """k_gemm_pass lowering (c64 default): load layout, GEMMs on the column
+    qubits in matrix order, diagonal ops moved across / between GEMMs, 32x32b
+    and 16x256b read-out layouts -- emulated against the oracle."""
+    c = make()
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(c.num_qubits, Precision.SINGLE, c.gates)
+    infos = plan.passes()
+    gemm = [i for i in infos if i["kernel"] == "gemm"]
+    assert gemm, infos
+    got = emulate_reg(plan, c.num_qubits, "single")
+    assert np.abs(got - want).max() <= 1e-5
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+
+
+def test_gemm_plans_cover_diagonals_and_readouts():
+    layouts = set()
+    with_ops = 0
+    for _name, make in GEMM_CASES:
+        c = make()
+        plan = CircuitPlan(c.num_qubits, Precision.SINGLE, c.gates)
+        nat = plan.native
+        for p, info in enumerate(plan.passes()):
+            if info["kernel"] != "gemm":
+                continue
+            with_ops += info["num_kernel_ops"] > 0
+            for f in range(info["num_phases"]):
+                layouts.add(bool(nat.phase(p, f)["flags"] & 8))
+    assert with_ops > 0 and layouts == {False, True}
