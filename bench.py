@@ -9,8 +9,12 @@ One *step* = one full circuit: |0...0> preparation plus every planned pass of
 the fused circuit, inputs (the state) resident in HBM.  The default N=1
 workload is BASELINE config 2: the seeded 28-qubit layered circuit (973 gates,
 fused to 189 at width 2) in complex64.  ``value`` counts ORIGINAL (unfused)
-gates per second.  For N>1 the state is sharded over the ranks (top log2 N
-qubits global) -- weak scaling: n = 28 + log2 N.
+gates per second.  The same JSON line carries ``configs``: BASELINE configs 3
+(qft-30 c128) and 4 (layered-33 c128, 128 GiB) measured in the same run.  For
+N>1 the state is sharded over the ranks (top log2 N qubits global) -- weak
+scaling on the north star's sharded curve: n = 33 + log2 N c64 (N = 8 is
+BASELINE config 5, 36 qubits), with the NVLink fraction of the swaps against
+a peer bandwidth measured in the same run.
 
 ``--impl reference`` times the reference's NumPy algorithm (the oracle port in
 oracle/, single-threaded like ref engines.py:190-203) on a bounded sample of the
@@ -57,6 +61,9 @@ def parse_args():
     ap.add_argument("--tensor-cores", type=int, default=0, help="1 on, -1 off, 0 default")
     ap.add_argument("--tc-min-dense", type=int, default=0)
     ap.add_argument("--streams", type=int, default=0, help="tile streams per CTA (0 default)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other single-GPU BASELINE configs (qft-30 / layered-33 c128)")
+    ap.add_argument("--config-steps", type=int, default=3, help="timed steps of each extra config")
     return ap.parse_args()
 
 
@@ -68,7 +75,9 @@ def workload(args, world: int):
     extra = int(round(math.log2(world))) if world > 1 else 0
     cfg = args.config or "layered28"
     if cfg == "layered28":
-        n, kind, prec = 28 + extra, "layered", "single"
+        # N = 1: BASELINE config 2 (28 q); N > 1: the north star's sharded
+        # curve, 33 + log2 N qubits c64 (N = 8 is config 5, 36 q)
+        n, kind, prec = (28 if world == 1 else 33 + extra), "layered", "single"
     elif cfg == "qft30":
         n, kind, prec = 30 + extra, "qft", "double"
     elif cfg == "layered33":
@@ -142,17 +151,28 @@ class ClockSampler:
 
 
 def plan_kernels(plan) -> str:
-    """Kernel(s) the plan launches (register-phase / shared-memory / tensor-core)."""
+    """Kernel(s) the plan launches."""
     names = set()
     for p in range(plan.num_passes):
         info = plan.native.pass_info(p)
-        mma = info["num_tc"] and any(plan.native.phase(p, f)["mma"] for f in range(info["num_phases"]))
         tb = info["tile_bits"] - info["reg_bits"]
-        tcn = ("+tcgen05" if tb == 7 else "+mma.sync") if mma else ""
-        names.add("k_tc_pass" if info["num_tc"] and not mma else
-                  f"k_reg_pass<RB={info['reg_bits']},TB={tb}>{tcn}" if info["reg_bits"]
-                  else "k_tile_pass")
+        if info["kernel"] == "gemm":
+            names.add(f"k_gemm_pass<{info['streams']}>+tcgen05")
+        elif info["kernel"] == "reg_tc":
+            names.add(f"k_reg_pass<RB={info['reg_bits']},TB={tb}>+" + ("tcgen05" if tb == 7 else "mma.sync"))
+        elif info["kernel"] == "reg":
+            names.add(f"k_reg_pass<RB={info['reg_bits']},TB={tb}>")
+        else:
+            names.add("k_tile_pass")
     return "+".join(sorted(names))
+
+
+def tensor_flops(plan, n: int) -> float:
+    """Tensor-core flops of one plan execution: each GEMM phase multiplies every
+    amplitude's 64-real row by a 64 x 64 real block in three fp16 products
+    (hi.hi + lo.hi + hi.lo): 3 x 2 x 64 x 2 flops per complex amplitude."""
+    gemms = sum(plan.native.pass_info(p)["num_tc"] for p in range(plan.num_passes))
+    return gemms * float(1 << n) * 3 * 2 * 64 * 2
 
 
 def measured_traffic(cfg: str, prec: str, n: int):
@@ -175,6 +195,17 @@ def measured_peak_hbm():
             return float(json.load(fh)["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def measured_peak_tensor():
+    """Dense fp16/bf16 tensor-core peak (MEASURED_PEAKS.json burst figure: a
+    pass is a short kernel), else the profiling recipe's nominal 2250."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["bf16_tflops"]), "measured"
+    except Exception:
+        return 2250.0, "fallback"
 
 
 def cpu_baseline(circuit_fused, g0: int, n: int, prec: str, budget_s: float = 20.0) -> dict:
@@ -288,62 +319,17 @@ def run_b200(args):
     if world > 1:
         return run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world, local)
 
-    plan = eng.plan(fused, precision)
-    n_passes = plan.num_passes
-    state = eng.init_state(n, precision)
+    m = measure(eng, fused, g0, n, precision, args.steps, args.warmup, args.pass_times)
+    plan, n_passes, pass_ms, ms_step = m["plan"], m["n_passes"], m["pass_ms"], m["ms_step"]
+    m_norm, m_clk = m["norm"], m["clocks"]
+    value = g0 / (ms_step / 1e3)
+    amp_bytes = precision.amplitude_bytes
+    pc = prec_code(precision)
+    state = m["state"]
     stream = torch.cuda.current_stream()
     s = stream.cuda_stream
-    import ctypes as C
-    from paper_2604_03816_b200 import _native
-    L = _native.lib()
-    pc = prec_code(precision)
-    amp_bytes = precision.amplitude_bytes
-
-    def step(events=None):
-        _native.check(L.svb_fill_basis(C.c_void_p(state.tensor.data_ptr()), n, pc, 0, C.c_void_p(s)))
-        if events is None:
-            plan.execute(state.tensor, s)
-        else:
-            for p in range(n_passes):
-                events[p][0].record(stream)
-                plan.execute(state.tensor, s, p, 1)
-                events[p][1].record(stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(n_passes)] for _ in range(args.steps)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        start.record(stream)
-        for k in range(args.steps):
-            step(ev[k])
-        stop.record(stream)
-        torch.cuda.synchronize()
-    total_ms = start.elapsed_time(stop)
-    pass_ms = [sum(ev[k][p][0].elapsed_time(ev[k][p][1]) for k in range(args.steps)) / args.steps
-               for p in range(n_passes)]
-    if args.pass_times:
-        for p_, ms_ in enumerate(pass_ms):
-            info = plan.native.pass_info(p_)
-            ops = [plan.native.kernel_op(p_, i)["kind"][0] + str(plan.native.kernel_op(p_, i)["k"])
-                   for i in range(info["num_kernel_ops"])]
-            fl = [plan.native.phase(p_, f)["flags"] for f in range(info["num_phases"])]
-            print(f"pass {p_:3d} {ms_:.3f} ms frac {2 * (1 << n) * precision.amplitude_bytes / ms_ / 1e6 / 6548:.2f} "
-                  f"L={info['low_bits']} high={info['high']} phases={info['num_phases']} flags={fl} "
-                  f"ops={ops} est={info['est_cost']:.2f}", file=sys.stderr)
-    ms_step = total_ms / args.steps
-    value = g0 / (ms_step / 1e3)
-    norm = eng.norm_squared(state)
-
-    # roofline of the dominant kernel (k_tile_pass): algorithmic bytes per launch
-    bytes_per_pass = 2 * (1 << n) * amp_bytes
-    avg_pass_ms = sum(pass_ms) / n_passes
-    achieved = bytes_per_pass / (avg_pass_ms / 1e3) / 1e9
     peak, peak_kind = measured_peak_hbm()
-    best_pass = min(pass_ms)
+    bytes_per_pass = 2 * (1 << n) * amp_bytes
 
     # single-gate pass (the north star's "per local gate pass"): one dense 2q
     # gate = one HBM round trip of the state with no compute to hide, timed
@@ -367,42 +353,78 @@ def run_b200(args):
                  "frac": bytes_per_pass / (gate_ms / 1e3) / 1e9 / peak}
 
     # e2e: public API from a host circuit: plan + launch (kernel-parameter H2D) +
-    # run + device->host read of the result (norm^2 and amplitude 0)
+    # run + device->host read of the result (norm^2 and amplitude 0).  Warm:
+    # the content-keyed plan cache hits (the serving case); cold: a fresh
+    # engine, so the native planner runs inside the timed region.
     eng.release(state)
-    del state
+    del state, m
     torch.cuda.empty_cache()
-    e2e_times = []
     h2d = n_passes * PASS_ARGS_BYTES  # __grid_constant__ parameter block per launch
-    for k in range(max(2, min(args.steps, 5)) + 1):
+
+    def e2e_once(engine):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        st = eng.run_circuit(fused, precision)
-        nrm = eng.norm_squared(st)
-        a0 = complex(st.tensor[0].item())
+        st = engine.run_circuit(fused, precision)
+        engine.norm_squared(st)
+        complex(st.tensor[0].item())
         dt = time.perf_counter() - t0
-        eng.release(st)
-        del st
+        engine.release(st)
+        return dt
+
+    e2e_times = []
+    for k in range(max(2, min(args.steps, 5)) + 1):
+        dt = e2e_once(eng)
         if k:
             e2e_times.append(dt)
     e2e_value = g0 / statistics.median(e2e_times)
+    cold_times = [e2e_once(B200Engine("b200-cold", device=local, options=eng.options)) for _ in range(2)]
+    torch.cuda.empty_cache()
 
-    # compute roofline of the same launches: algorithmic flops of the fused
+    # compute rooflines of the same launches: algorithmic flops of the fused
     # gates (dense k-qubit: 8*2^k - 2 real flops per amplitude, diagonal: 6)
-    # against the vector FMA peak of the precision (FP32 128 / FP64 64 FMA per
-    # clock per SM at the sampled max SM clock)
+    # against the vector FMA peak, and the tensor-core flops the GEMM phases
+    # issue against the measured dense fp16 peak
     from paper_2604_03816_b200.circuit import effective_unitary as _eu
     flops_amp = 0
     for op in fused.gates:
         u = _eu(op)
         k = len(op.targets)
         flops_amp += 6 if np.count_nonzero(u - np.diag(np.diag(u))) == 0 else 8 * (1 << k) - 2
-    clk_summary = clk.summary()
-    sm_mhz = clk_summary.get("sm_max_mhz") or 1965.0
+    sm_mhz = (m_clk or {}).get("sm_max_mhz") or 1965.0
     fma_per_clk = 128 if prec == "single" else 64
     dev_props = torch.cuda.get_device_properties(local)
     peak_tflops = dev_props.multi_processor_count * fma_per_clk * 2 * sm_mhz * 1e6 / 1e12
     achieved_tflops = flops_amp * (1 << n) / (sum(pass_ms) / 1e3) / 1e12
+    tc_flops = tensor_flops(plan, n)
+    tpeak, tpeak_kind = measured_peak_tensor()
     traffic = measured_traffic(cfg, prec, n)
+    avg_pass_ms = sum(pass_ms) / n_passes
+    achieved = bytes_per_pass / (avg_pass_ms / 1e3) / 1e9
+    best_pass = min(pass_ms)
+
+    # the other single-GPU BASELINE configs (3: qft-30 c128, 4: layered-33 c128)
+    configs = {}
+    if cfg == "layered28" and not args.no_configs:
+        for name, circ, pr in (("qft30_c128", gen_circuit("qft", 30), "double"),
+                               ("layered33_c128", gen_circuit("layered", 33), "double")):
+            f2, _ = fuse(circ, args.fuse_width)
+            ng0 = len(circ.gates)
+            mm = measure(B200Engine("b200-cfg", device=local, options=eng.options), f2, ng0, circ.num_qubits,
+                         Precision(pr), args.config_steps, 3, False)
+            b2 = 2 * (1 << circ.num_qubits) * Precision(pr).amplitude_bytes
+            apm = sum(mm["pass_ms"]) / mm["n_passes"]
+            configs[name] = {"workload": f"{circ.name} {pr}, fused {ng0}->{len(f2.gates)}",
+                             "value": ng0 / (mm["ms_step"] / 1e3), "unit": "gates/s",
+                             "ms_per_step": mm["ms_step"], "steps": args.config_steps, "warmup": 3,
+                             "passes": mm["n_passes"], "kernel": plan_kernels(mm["plan"]),
+                             "roofline": {"bound": "hbm", "achieved": b2 / (apm / 1e3) / 1e9, "peak": peak,
+                                          "unit": "GB/s", "frac": b2 / (apm / 1e3) / 1e9 / peak,
+                                          "peak_kind": peak_kind, "avg_launch_ms": apm,
+                                          "traffic": measured_traffic(name.split("_")[0], pr, circ.num_qubits)},
+                             "norm_after": mm["norm"], "clocks": mm["clocks"]}
+            eng_state = mm.pop("state")
+            del eng_state, mm
+            torch.cuda.empty_cache()
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -421,28 +443,130 @@ def run_b200(args):
                    "precision_decision": decision.rationale + " (bench forces "
                    + prec + " as BASELINE config names it)",
                    "circuit_ms": ms_step, "fused_gates_per_s": gf / (ms_step / 1e3),
-                   "passes_per_s": n_passes / (ms_step / 1e3), "norm_after": norm},
+                   "passes_per_s": n_passes / (ms_step / 1e3), "norm_after": m_norm},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": plan_kernels(plan), "bytes_per_launch": bytes_per_pass,
                      "avg_launch_ms": avg_pass_ms, "best_launch_ms": best_pass,
                      "best_frac": bytes_per_pass / (best_pass / 1e3) / 1e9 / peak,
+                     "pass_ms": [round(x, 4) for x in pass_ms],
                      "single_gate_pass": gate_pass,
+                     "tensor": {"achieved": tc_flops / (sum(pass_ms) / 1e3) / 1e12, "peak": tpeak,
+                                "unit": "TFLOP/s", "peak_kind": tpeak_kind,
+                                "frac": tc_flops / (sum(pass_ms) / 1e3) / 1e12 / tpeak,
+                                "flops_per_step": tc_flops,
+                                "note": "fp16 tcgen05 GEMM phases: 3 products (hi.hi, lo.hi, hi.lo) of a "
+                                        "64x64 real block per amplitude row"},
                      "compute": {"bound": "fp32-fma" if prec == "single" else "fp64-fma",
                                  "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                                  "frac": achieved_tflops / peak_tflops,
                                  "flops_per_amp": flops_amp,
-                                 "note": "vector FMA peak = SMs x FMA/clk x 2 x max SM clock; "
-                                         "the passes are HBM- or FMA-bound, whichever is larger"}},
+                                 "note": "algorithmic gate flops vs the vector FMA peak (SMs x FMA/clk x "
+                                         "2 x max SM clock); c64 GEMM phases run on the tensor cores "
+                                         "(see roofline.tensor), so this is a reference line there"}},
+        "configs": configs,
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8 + (8 if pc == 0 else 16),
-                "path": "B200Engine.run_circuit(fused circuit; plan cached by content after the first, untimed call) + norm_squared + amplitude[0] read"},
+                "path": "B200Engine.run_circuit(fused circuit; plan cached by content after the first, "
+                        "untimed call) + norm_squared + amplitude[0] read",
+                "cold": {"value": g0 / statistics.median(cold_times), "unit": "gates/s",
+                         "path": "same call on a fresh engine: native planning inside the timed region"}},
         "gpu_launches": args.steps * (n_passes + 2),
-        "clocks": clk_summary,
+        "clocks": m_clk,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
     return 0
+
+
+def gen_circuit(kind: str, n: int):
+    from paper_2604_03816_b200 import generators as gen
+    return gen.layered_circuit(n) if kind == "layered" else gen.qft_circuit(n)
+
+
+def measure(eng, fused, g0: int, n: int, precision, steps: int, warmup: int, pass_times: bool = False) -> dict:
+    """Device time of `steps` circuit executions (|0> preparation + every pass),
+    CUDA events around the whole timed region and around each pass, clocks
+    sampled during it."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_03816_b200 import _native
+    from paper_2604_03816_b200.b200 import prec_code
+    plan = eng.plan(fused, precision)
+    n_passes = plan.num_passes
+    state = eng.init_state(n, precision)
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    L = _native.lib()
+    pc = prec_code(precision)
+
+    def step(events=None):
+        _native.check(L.svb_fill_basis(C.c_void_p(state.tensor.data_ptr()), n, pc, 0, C.c_void_p(s)))
+        if events is None:
+            plan.execute(state.tensor, s)
+        else:
+            for p in range(n_passes):
+                events[p][0].record(stream)
+                plan.execute(state.tensor, s, p, 1)
+                events[p][1].record(stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_passes)] for _ in range(steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for k in range(steps):
+            step(ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    total_ms = start.elapsed_time(stop)
+    pass_ms = [sum(ev[k][p][0].elapsed_time(ev[k][p][1]) for k in range(steps)) / steps
+               for p in range(n_passes)]
+    if pass_times:
+        for p_, ms_ in enumerate(pass_ms):
+            info = plan.native.pass_info(p_)
+            ops = [plan.native.kernel_op(p_, i)["kind"][0] + str(plan.native.kernel_op(p_, i)["k"])
+                   for i in range(info["num_kernel_ops"])]
+            fl = [plan.native.phase(p_, f)["flags"] for f in range(info["num_phases"])]
+            print(f"pass {p_:3d} {ms_:.3f} ms frac {2 * (1 << n) * precision.amplitude_bytes / ms_ / 1e6 / 6445:.2f} "
+                  f"{info['kernel']} L={info['low_bits']} high={info['high']} phases={info['num_phases']} "
+                  f"gemms={info['num_tc']} flags={fl} conf={info['bank_conflicts']} ops={ops}", file=sys.stderr)
+    return {"plan": plan, "n_passes": n_passes, "pass_ms": pass_ms, "ms_step": total_ms / steps,
+            "state": state, "norm": eng.norm_squared(state), "clocks": clk.summary()}
+
+
+def p2p_peak_gbs(dist, red_dev, local) -> float:
+    """Peer bandwidth per direction measured here: every rank sends 1 GiB to and
+    receives 1 GiB from rank ^ 1 (NCCL over NVLink), best of 3, min over ranks."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    peer = rank ^ 1
+    if peer >= world:
+        return None
+    a = torch.empty(1 << 27, dtype=torch.float64, device=f"cuda:{local}")
+    b = torch.empty_like(a)
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, a, peer), dist.P2POp(dist.irecv, b, peer)]):
+            r.wait()
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, a.numel() * 8 / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    t = torch.tensor([best], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    del a, b
+    torch.cuda.empty_cache()
+    return float(t.item())
 
 
 def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world, local):
@@ -507,7 +631,7 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
     achieved = bytes_per_pass * n_passes / (local_ms / 1e3) / 1e9 if n_passes else 0.0
     sent = sum((1 - 2.0 ** -s_.m) * (1 << n_local) * amp_bytes for s_ in swaps)
     nvl = sent / (swap_ms / 1e3) / 1e9 if swap_ms > 0 else None
-
+    nvl_peak = p2p_peak_gbs(dist, red_dev, local) if dist.get_backend() == "nccl" else None
     # e2e through the public sharded API (schedule + plan + run + all-reduced norm)
     e2e = []
     for k in range(3):
@@ -539,7 +663,9 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                          "kernel": "k_reg_pass (local passes)",
                          "nvlink": {"bytes_sent_per_gpu": sent, "achieved_gbs": nvl,
-                                    "peak_gbs": 770.0, "frac": (nvl / 770.0) if nvl else None}},
+                                    "peak_gbs": nvl_peak,
+                                    "peak_kind": "measured: 1 GiB pairwise send/recv, max over ranks",
+                                    "frac": (nvl / nvl_peak) if (nvl and nvl_peak) else None}},
             "e2e": {"value": g0 / statistics.median(e2e), "unit": "gates/s",
                     "h2d_bytes_per_step": n_passes * PASS_ARGS_BYTES, "d2h_bytes_per_step": 8},
             "gpu_launches": args.steps * (n_passes + 2),

@@ -87,12 +87,50 @@ class CircuitPlan:
         self.native.execute(tensor.data_ptr(), stream, first, count)
 
 
+D2H_CHUNK_BYTES = 1 << 30
+
+
+def d2h_chunked(tensor, out: np.ndarray, chunk_bytes: int = D2H_CHUNK_BYTES) -> np.ndarray:
+    """Copy a device tensor into the host array ``out`` in <= ``chunk_bytes``
+    pieces through two pinned staging buffers on a side stream: the D2H of
+    chunk i + 1 overlaps the host copy of chunk i.  Host memory beyond ``out``
+    is two chunks, whatever the state size (a 33-qubit c128 state is 128 GiB;
+    ``tensor.cpu()`` would allocate a second full pageable copy)."""
+    import torch
+    n = tensor.numel()
+    per = max(1, chunk_bytes // tensor.element_size())
+    flat = torch.from_numpy(out.reshape(-1))
+    dev = tensor.device
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    bufs = [torch.empty(min(per, n), dtype=tensor.dtype, pin_memory=True) for _ in range(2 if n > per else 1)]
+    pending = None
+    for k, c0 in enumerate(range(0, n, per)):
+        c1 = min(n, c0 + per)
+        buf = bufs[k % len(bufs)]
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(side):
+            buf[:c1 - c0].copy_(tensor[c0:c1], non_blocking=True)
+            ev.record(side)
+        if pending is not None:
+            pev, pbuf, p0, p1 = pending
+            pev.synchronize()
+            flat[p0:p1].copy_(pbuf[:p1 - p0])
+        pending = (ev, buf, c0, c1)
+    if pending is not None:
+        pev, pbuf, p0, p1 = pending
+        pev.synchronize()
+        flat[p0:p1].copy_(pbuf[:p1 - p0])
+    return out
+
+
 class DeviceStateVector:
     """A state whose amplitudes live in HBM.
 
     ``amplitudes`` materialises a host numpy copy lazily (cached until the next
     device mutation), matching the reference contract that callers re-read
-    ``amplitudes`` after gates (ref circuit.py:189-194).  ``norm_squared`` and
+    ``amplitudes`` after gates (ref circuit.py:189-194); the copy is chunked
+    and pinned-double-buffered (``d2h_chunked``).  ``norm_squared`` and
     ``probabilities`` run on the device in FP64 accumulation.
     """
 
@@ -112,7 +150,9 @@ class DeviceStateVector:
     def amplitudes(self) -> np.ndarray:
         if self._host is None or self._host_version != self._version:
             self._engine.synchronize()
-            self._host = self.tensor.cpu().numpy()
+            self._host = None  # drop the stale copy before allocating the new one
+            out = np.empty(self.tensor.numel(), dtype=as_precision(self.precision).dtype)
+            self._host = d2h_chunked(self.tensor, out)
             self._host_version = self._version
         return self._host
 
@@ -322,9 +362,18 @@ class B200Engine(EngineBase):
         values, counts = np.unique(host, return_counts=True)
         return SampleResult({format(int(v), f"0{n}b"): int(c) for v, c in zip(values, counts)}, shots)
 
-    def probabilities(self, state: DeviceStateVector) -> np.ndarray:
-        out = torch.empty(1 << state.num_qubits, dtype=torch.float64, device=state.tensor.device)
-        _native.check(_native.lib().svb_probabilities(
-            C.c_void_p(state.tensor.data_ptr()), prec_code(state.precision), 0,
-            1 << state.num_qubits, C.c_void_p(out.data_ptr()), C.c_void_p(self.stream())))
-        return out.cpu().numpy()
+    def probabilities(self, state: DeviceStateVector, chunk_bytes: int = D2H_CHUNK_BYTES) -> np.ndarray:
+        """|amp|^2 in FP64 (ref circuit.py:203-205), computed on the device one
+        chunk at a time into a reusable buffer and copied into the host array:
+        no 2^n-double device array next to a near-HBM-sized state."""
+        n = 1 << state.num_qubits
+        out = np.empty(n, dtype=np.float64)
+        per = max(1, min(n, chunk_bytes // 8))
+        dev_buf = torch.empty(per, dtype=torch.float64, device=state.tensor.device)
+        for c0 in range(0, n, per):
+            cnt = min(per, n - c0)
+            _native.check(_native.lib().svb_probabilities(
+                C.c_void_p(state.tensor.data_ptr()), prec_code(state.precision), c0, cnt,
+                C.c_void_p(dev_buf.data_ptr()), C.c_void_p(self.stream())))
+            d2h_chunked(dev_buf[:cnt], out[c0:c0 + cnt], chunk_bytes)
+        return out

@@ -52,8 +52,19 @@ __host__ __device__ __forceinline__ constexpr int ctz_c(int x) {
   return (x & 1) ? 0 : (x & 2) ? 1 : (x & 4) ? 2 : (x & 8) ? 3 : 4;
 }
 
+// Tile-invariant addressing, computed once per CTA (gemm_tables): the
+// thread parts and register bases of every layout change of the pass.
+struct GemmTables {
+  uint32_t wb[kMaxMmaPerPass][128];   // [p][thread] A word of register 0, layout p -> A of GEMM p + 1
+  uint32_t wr[kMaxMmaPerPass][8];     // [p][register bit] A word offsets (uniform)
+  uint32_t ld[128];                   // [thread] tile index of register 0 in the load layout
+  uint32_t ldr[8];                    // load layout: tile index offsets of the register bits
+  long long st[128];                  // [thread] shard offset of register 0 in the last layout
+  long long str[8];                   // last layout: shard offsets of the register bits
+};
+
 struct GemmSmem {
-  size_t pool, dthr, dout, red, mats, tiles, total;
+  size_t pool, dthr, dout, red, tabs, mats, tiles, total;
 };
 __host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng) {
   GemmSmem l;
@@ -61,7 +72,8 @@ __host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(float2), 128);
   l.dout = l.dthr + align_up(size_t(h.n_ops) * 128, 128);
   l.red = l.dout + align_up(size_t(ng) * 2 * kMaxOps * sizeof(int), 128);
-  l.mats = align_up(l.red + size_t(ng) * 8 * sizeof(float), 1024);
+  l.tabs = align_up(l.red + size_t(ng) * 8 * sizeof(float), 128);
+  l.mats = align_up(l.tabs + sizeof(GemmTables), 1024);
   l.tiles = l.mats + size_t(h.tc_count) * kMmaMatBytes;
   l.total = l.tiles + size_t(ng) * kGemmTileBytes;
   return l;
@@ -90,32 +102,6 @@ __device__ __forceinline__ void gemm_split_store(uint32_t* __restrict__ A, uint3
   A[w + kGemmAWords] = pack_half2(xr - hf.x, xi - hf.y);
 }
 
-// Word address (in A of the phase whose table is `wt`) of the element held in
-// register 0 by this thread (layout `map`): XOR over the set thread bits.
-__device__ __forceinline__ uint32_t gemm_wbase(const PhaseDesc& cur, const unsigned short* wt, int gt) {
-  uint32_t w = 0;
-#pragma unroll
-  for (int b = 0; b < 7; ++b)
-    if ((gt >> b) & 1) w ^= wt[cur.map[5 + b]];
-  return w;
-}
-
-// Convert the 32 registers (layout `cur`) into the A operand of the next GEMM
-// (word table `wt`), visiting registers in Gray-code order: one XOR each.
-__device__ __forceinline__ void gemm_write_a(uint32_t* __restrict__ A, const float2 (&v)[32], const PhaseDesc& cur,
-                                             const unsigned short* wt, int gt) {
-  uint32_t basis[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) basis[i] = wt[cur.map[i]];
-  uint32_t w = gemm_wbase(cur, wt, gt);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    if (i) w ^= basis[ctz_c(i)];
-    const int r = i ^ (i >> 1);
-    gemm_split_store(A, w, v[r].x, v[r].y);
-  }
-}
-
 // tcgen05.ld 16x256b, 8 repetitions: 16 TMEM lanes x 64 columns per warp;
 // thread t gets rows t/4 and t/4 + 8, columns 8c + 2 (t % 4) + {0, 1}
 __device__ __forceinline__ void t5_ld16x256_x8(uint32_t taddr, uint32_t (&d)[32]) {
@@ -137,9 +123,10 @@ __device__ __forceinline__ void t5_ld16x256_x8(uint32_t taddr, uint32_t (&d)[32]
 //    half; lanes = j0 j1 | row bits 0..2 -- two column bits on the lanes,
 //    which lets the planner put low tile qubits there (coalesced stores,
 //    conflict-free A writes).
-__device__ __forceinline__ void gemm_read_half(uint32_t dcol, bool ld16, int half, float2 (&u)[16]) {
+template <bool LD16>
+__device__ __forceinline__ void gemm_read_half(uint32_t dcol, int half, float2 (&u)[16]) {
   uint32_t d[32];
-  if (!ld16) {
+  if constexpr (!LD16) {
     t5_ld32(dcol + 32u * half, d);
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
@@ -165,13 +152,14 @@ __device__ __forceinline__ void gemm_diag_half(float2 (&u)[16], const OpDesc& op
   for (int q = 0; q < 16; ++q) u[q] = cmul(u[q], table[dbase | rmap[q | half << 4]]);
 }
 
-// Convert one half into the A operand of the next GEMM (word table `wt`).
-__device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const float2 (&u)[16], const PhaseDesc& cur,
-                                                const unsigned short* wt, int gt, int half) {
+// Convert one half into the A operand of the next GEMM: word of register rho
+// = wbase ^ XOR of wr[bit] over rho's bits, visited in Gray-code order.
+__device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const float2 (&u)[16], uint32_t wbase,
+                                                const uint32_t* __restrict__ wr, int half) {
   uint32_t basis[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) basis[i] = wt[cur.map[i]];
-  uint32_t w = gemm_wbase(cur, wt, gt) ^ (half ? uint32_t(wt[cur.map[4]]) : 0u);
+  for (int i = 0; i < 4; ++i) basis[i] = wr[i];
+  uint32_t w = wbase ^ (half ? wr[4] : 0u);
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     if (i) w ^= basis[ctz_c(i)];
@@ -180,11 +168,105 @@ __device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const 
   }
 }
 
-__device__ __forceinline__ float norm2_16(const float2 (&u)[16]) {
-  float s = 0.f;
+// One tile's GEMM-phase epilogue with a compile-time read-out shape: D ->
+// registers -> diagonal ops -> hi/lo A words of the next GEMM.
+template <bool LD16>
+__device__ __forceinline__ void gemm_phase_body(uint32_t* __restrict__ A, uint32_t dcol, const PassArgs<float2>& args,
+                                                const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
+                                                const int* dslot, int gt, uint32_t wbase, const uint32_t* wr) {
+  constexpr int NTG = 128;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) s = fmaf(u[q].x, u[q].x, fmaf(u[q].y, u[q].y, s));
-  return s;
+  for (int half = 0; half < 2; ++half) {
+    float2 u[16];
+    gemm_read_half<LD16>(dcol, half, u);
+    for (int o = ph.op_begin; o < ph.op_end; ++o)
+      gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
+                     int(dthr[o * NTG + gt]) | (args.h.has_outside ? dslot[o] : 0), half);
+    gemm_write_half(A, u, wbase, wr, half);
+  }
+}
+
+template <bool LD16>
+__device__ __forceinline__ float gemm_norm_body(uint32_t dcol) {
+  float w = 0.f;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float2 u[16];
+    gemm_read_half<LD16>(dcol, half, u);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w = fmaf(u[q].x, u[q].x, fmaf(u[q].y, u[q].y, w));
+  }
+  return w;
+}
+
+// Final store of one tile (last layout): diagonal ops, undo the scale /
+// restore the norm (factor f), 16-byte stores when register bit 0 is tile
+// bit 0 (`pairs`), else 8-byte.
+template <bool LD16>
+__device__ __forceinline__ void gemm_store_body(float2* __restrict__ dst, uint32_t dcol, const PassArgs<float2>& args,
+                                                const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
+                                                const int* dslot, int gt, const long long* __restrict__ sr,
+                                                float f, bool pairs) {
+  constexpr int NTG = 128;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float2 u[16];
+    gemm_read_half<LD16>(dcol, half, u);
+    for (int o = ph.op_begin; o < ph.op_end; ++o)
+      gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
+                     int(dthr[o * NTG + gt]) | (args.h.has_outside ? dslot[o] : 0), half);
+    long long goff[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) goff[i] = sr[i];
+    long long o = half ? sr[4] : 0;
+    if (pairs) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i) {
+          const int b = ctz_c(i) + 1;
+          o += (((i ^ (i >> 1)) << 1) >> b) & 1 ? goff[b] : -goff[b];
+        }
+        const int r = (i ^ (i >> 1)) << 1;
+        *reinterpret_cast<float4*>(dst + o) = make_float4(u[r].x * f, u[r].y * f, u[r | 1].x * f, u[r | 1].y * f);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i) {
+          const int b = ctz_c(i);
+          o += ((i ^ (i >> 1)) >> b) & 1 ? goff[b] : -goff[b];
+        }
+        const int r = i ^ (i >> 1);
+        dst[o] = make_float2(u[r].x * f, u[r].y * f);
+      }
+    }
+  }
+}
+
+// Address tables of the pass (threads 0..127 compute them once per CTA).
+__device__ __forceinline__ void gemm_tables(GemmTables& t, const PassArgs<float2>& args, int gt) {
+  const PassHeader& h = args.h;
+  const int P = h.n_phases - 1;
+  for (int p = 0; p < P; ++p) {
+    const PhaseDesc& cur = args.phases[p];
+    const unsigned short* wt = reinterpret_cast<const unsigned short*>(args.phases[p + 1].R);
+    uint32_t w = 0;
+    for (int b = 0; b < 7; ++b)
+      if ((gt >> b) & 1) w ^= wt[cur.map[5 + b]];
+    t.wb[p][gt] = w;
+    if (gt < 5) t.wr[p][gt] = wt[cur.map[gt]];
+  }
+  const PhaseDesc& p0 = args.phases[0];
+  uint32_t x = 0;
+  for (int b = 0; b < 7; ++b) x |= uint32_t((gt >> b) & 1) << p0.map[5 + b];
+  t.ld[gt] = x;
+  if (gt < 5) t.ldr[gt] = 1u << p0.map[gt];
+  const PhaseDesc& pl = args.phases[P];
+  long long g = 0;
+  for (int b = 0; b < 7; ++b)
+    if ((gt >> b) & 1) g += 1LL << gpos(pl.map[5 + b], h);
+  t.st[gt] = g;
+  if (gt < 5) t.str[gt] = 1LL << gpos(pl.map[gt], h);
 }
 
 template <int NG>
@@ -232,6 +314,8 @@ __global__ void __launch_bounds__(NG * 128, 1)
     const OpDesc& op = args.ops[e / NTG];
     dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
   }
+  GemmTables& tab = *reinterpret_cast<GemmTables*>(smem + lay.tabs);
+  if (tid < NTG) gemm_tables(tab, args, tid);
   fence_proxy_async_smem();  // B operands written by the generic proxy, read by the tensor core
   t5_fence_before();
   __syncthreads();
@@ -284,19 +368,18 @@ __global__ void __launch_bounds__(NG * 128, 1)
     mbar_wait(&full[group], fpar);
     fpar ^= 1;
 
-    // ---- phase 0: linear tile -> registers (load layout), ops_0, tile norm
+    // ---- phase 0: linear tile -> registers (load layout), tile norm, scale,
+    // ops_0, A of GEMM 1 written in place
     float S, n2in;
     {
       float2 v[32];
       const PhaseDesc& p0 = args.phases[0];
-      uint32_t x = 0;
-#pragma unroll
-      for (int b = 0; b < 7; ++b) x |= uint32_t((gt >> b) & 1) << p0.map[5 + b];
+      uint32_t x = tab.ld[gt];
       if (p0.map[0] == 0) {
         // register bit 0 = tile bit 0: adjacent pairs, 16-byte loads
         uint32_t basis[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) basis[i] = 1u << p0.map[1 + i];
+        for (int i = 0; i < 4; ++i) basis[i] = tab.ldr[1 + i];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if (i) x ^= basis[ctz_c(i)];
@@ -308,7 +391,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
       } else {
         uint32_t basis[5];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) basis[i] = 1u << p0.map[i];
+        for (int i = 0; i < 5; ++i) basis[i] = tab.ldr[i];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           if (i) x ^= basis[ctz_c(i)];
@@ -325,6 +408,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
       const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
       const int se = min(max(268 - ebits, 1), 253);
       S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
+      const uint32_t wb0 = tab.wb[0][gt];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float2 u[16];
@@ -333,7 +417,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
         for (int o = p0.op_begin; o < p0.op_end; ++o)
           gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
                          int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
-        gemm_write_half(A, u, p0, reinterpret_cast<const unsigned short*>(args.phases[1].R), gt, half);
+        gemm_write_half(A, u, wb0, tab.wr[0], half);
       }
     }
     fence_proxy_async_smem();
@@ -362,15 +446,10 @@ __global__ void __launch_bounds__(NG * 128, 1)
       mpar ^= 1;
       t5_fence_after();
       if (p < P) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float2 u[16];
-          gemm_read_half(dcol, ld16, half, u);
-          for (int o = ph.op_begin; o < ph.op_end; ++o)
-            gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
-                           int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
-          gemm_write_half(A, u, ph, reinterpret_cast<const unsigned short*>(args.phases[p + 1].R), gt, half);
-        }
+        if (ld16)
+          gemm_phase_body<true>(A, dcol, args, ph, pool, dthr, dslot, gt, tab.wb[p][gt], tab.wr[p]);
+        else
+          gemm_phase_body<false>(A, dcol, args, ph, pool, dthr, dslot, gt, tab.wb[p][gt], tab.wr[p]);
         fence_proxy_async_smem();
         t5_fence_before();
         group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
@@ -381,13 +460,7 @@ __global__ void __launch_bounds__(NG * 128, 1)
       if (wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
       // tile 2-norm of the result (diagonal ops are unimodular: applied after)
       {
-        float w = 0.f;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float2 u[16];
-          gemm_read_half(dcol, ld16, half, u);
-          w += norm2_16(u);
-        }
+        float w = ld16 ? gemm_norm_body<true>(dcol) : gemm_norm_body<false>(dcol);
 #pragma unroll
         for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
         if (lane == 0) red[group * 8 + 4 + wig] = w;
@@ -396,45 +469,12 @@ __global__ void __launch_bounds__(NG * 128, 1)
       const float n2out = red[group * 8 + 4] + red[group * 8 + 5] + red[group * 8 + 6] + red[group * 8 + 7];
       // undo the scale, restore the tile 2-norm (all ops unitary)
       const float f = n2out > 0.f ? sqrtf(n2in * S * S / n2out) / S : 1.f / S;
-      long long g = 0;
-#pragma unroll
-      for (int b = 0; b < 7; ++b)
-        if ((gt >> b) & 1) g += 1LL << gpos(ph.map[5 + b], h);
-      float2* __restrict__ dst = amps + origin + g;
+      float2* __restrict__ dst = amps + origin + tab.st[gt];
       const bool pairs = ph.map[0] == 0;  // register bit 0 = tile bit 0: 16-byte stores
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float2 u[16];
-        gemm_read_half(dcol, ld16, half, u);
-        for (int o = ph.op_begin; o < ph.op_end; ++o)
-          gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
-                         int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
-        long long goff[5];
-#pragma unroll
-        for (int i = 0; i < 5; ++i) goff[i] = 1LL << gpos(ph.map[i], h);
-        long long o = half ? goff[4] : 0;
-        if (pairs) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i) {
-              const int b = ctz_c(i) + 1;
-              o += (((i ^ (i >> 1)) << 1) >> b) & 1 ? goff[b] : -goff[b];
-            }
-            const int r = (i ^ (i >> 1)) << 1;
-            *reinterpret_cast<float4*>(dst + o) = make_float4(u[r].x * f, u[r].y * f, u[r | 1].x * f, u[r | 1].y * f);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i) {
-              const int b = ctz_c(i);
-              o += ((i ^ (i >> 1)) >> b) & 1 ? goff[b] : -goff[b];
-            }
-            const int r = i ^ (i >> 1);
-            dst[o] = make_float2(u[r].x * f, u[r].y * f);
-          }
-        }
-      }
+      if (ld16)
+        gemm_store_body<true>(dst, dcol, args, ph, pool, dthr, dslot, gt, tab.str, f, pairs);
+      else
+        gemm_store_body<false>(dst, dcol, args, ph, pool, dthr, dslot, gt, tab.str, f, pairs);
       t5_fence_before();
     }
   }
