@@ -61,6 +61,7 @@ def parse_args():
     ap.add_argument("--tensor-cores", type=int, default=0, help="1 on, -1 off, 0 default")
     ap.add_argument("--tc-min-dense", type=int, default=0)
     ap.add_argument("--streams", type=int, default=0, help="tile streams per CTA (0 default)")
+    ap.add_argument("--gemm-warps", type=int, default=0, help="k_gemm_pass warps per tile stream (4/8)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other single-GPU BASELINE configs (qft-30 / layered-33 c128)")
     ap.add_argument("--config-steps", type=int, default=3, help="timed steps of each extra config")
@@ -313,7 +314,7 @@ def run_b200(args):
                         tile_bits=args.tile_bits, min_low_bits=args.min_low_bits,
                         reg_bits=args.reg_bits, no_reg_phases=int(args.no_reg_phases),
                         tensor_cores=args.tensor_cores, tc_min_dense=args.tc_min_dense,
-                        streams=args.streams)
+                        streams=args.streams, gemm_warps=args.gemm_warps)
     eng = B200Engine("b200-bench", device=local, options=opts)
 
     if world > 1:

@@ -70,6 +70,7 @@ typedef struct svb_plan_options {
                            groups of 128 threads (7 thread bits; 3-4 without a
                            producer warp), 1 = one stream of 256; 0 = default
                            (4 for c64 tensor-core phases, 3 for c128)           */
+  int gemm_warps;       /* k_gemm_pass warps per tile stream: 4 or 8 (0: default 8) */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */

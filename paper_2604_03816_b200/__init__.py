@@ -22,7 +22,7 @@ ENGINE_NAME = "b200"
 
 
 def _register() -> None:
-    eng = B200Engine(ENGINE_NAME)
+    eng = B200Engine(ENGINE_NAME, devices="all")  # shards over the box's GPUs when a state does not fit one
     if ENGINE_NAME not in {e.name for e in registered_engines()}:
         register_engine(eng)
     try:

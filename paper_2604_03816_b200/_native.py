@@ -35,7 +35,7 @@ class PlanOptions(C.Structure):
                 ("max_ops_per_pass", C.c_int), ("cost_budget", C.c_double),
                 ("no_diag_merge", C.c_int), ("stages", C.c_int), ("reg_bits", C.c_int),
                 ("no_reg_phases", C.c_int), ("tensor_cores", C.c_int), ("tc_min_dense", C.c_int),
-                ("no_window_search", C.c_int), ("streams", C.c_int)]
+                ("no_window_search", C.c_int), ("streams", C.c_int), ("gemm_warps", C.c_int)]
 
 
 class PassInfo(C.Structure):

@@ -164,13 +164,56 @@ class DeviceStateVector:
 
 
 class B200Engine(EngineBase):
-    """CUDA state-vector engine for sm_100a (registered as ``"b200"``)."""
+    """CUDA state-vector engine for sm_100a (registered as ``"b200"``).
+
+    ``devices`` (``None``: this engine's device only; ``"all"``: every visible
+    GPU; or a list of device indices, repeats allowed) lets a state that does
+    not fit one device be sharded over several -- the north star's replacement
+    for the reference's CPU fallback (ref memory.py:290-340).  ``shards``
+    forces a shard count (tests run several shards on one device)."""
 
     def __init__(self, name: str = "b200", *, capacity_bytes: int | None = None,
-                 device: int | str | torch.device | None = None, options=None):
+                 device: int | str | torch.device | None = None, options=None,
+                 devices=None, shards: int | None = None):
         super().__init__(name, requires_accelerator=True, capacity_bytes=capacity_bytes)
         self._device = device
         self.options = options
+        self._devices = devices
+        self._shards = shards
+        self._dev_engines: dict = {}
+
+    # ------------------------------------------------------------ sharding
+    def device_list(self) -> list:
+        if self._devices is None:
+            return [self.device.index if self.device.index is not None else torch.cuda.current_device()]
+        if self._devices == "all":
+            return list(range(torch.cuda.device_count()))
+        return [int(d) for d in self._devices]
+
+    def device_engine(self, dev: int) -> "B200Engine":
+        """Per-device engine used for one shard (own plan cache, own stream)."""
+        eng = self._dev_engines.get(dev)
+        if eng is None:
+            eng = B200Engine(f"{self.name}@{dev}", device=dev, options=self.options)
+            self._dev_engines[dev] = eng
+        return eng
+
+    def shard_devices(self, num_qubits: int, precision) -> list | None:
+        """Devices to shard a new state over, or None for one device."""
+        from . import multidevice as md
+        devs = self.device_list()
+        if self._shards:
+            if self._shards > len(devs) and len(set(devs)) == 1:
+                devs = devs * self._shards
+            return devs[:self._shards] if self._shards > 1 else None
+        if len(devs) < 2:
+            return None
+        world = md.plan_shards(self, num_qubits, precision, devs)
+        if world == -1:
+            requested = (1 << num_qubits) * as_precision(precision).amplitude_bytes
+            free = sum(torch.cuda.mem_get_info(d)[0] for d in sorted(set(devs)))
+            raise AllocationError(requested, free)
+        return devs[:world] if world > 1 else None
 
     # ---------------------------------------------------------------- plumbing
     @property
@@ -193,6 +236,8 @@ class B200Engine(EngineBase):
 
     def synchronize(self) -> None:
         torch.cuda.current_stream(self.device).synchronize()
+        for eng in self._dev_engines.values():
+            eng.synchronize()
 
     def _alloc(self, num_qubits: int, precision) -> torch.Tensor:
         if num_qubits < 1:
@@ -208,15 +253,41 @@ class B200Engine(EngineBase):
             raise AllocationError(requested, free) from None
 
     # ------------------------------------------------------------- Engine API
-    def init_state(self, num_qubits: int, precision=Precision.DOUBLE) -> DeviceStateVector:
+    def _check_capacity(self, num_qubits: int, precision) -> None:
+        if num_qubits < 1:
+            raise ValueError("num_qubits must be >= 1")
+        requested = (1 << num_qubits) * as_precision(precision).amplitude_bytes
+        if self.capacity_bytes is not None and requested >= self.capacity_bytes:
+            raise AllocationError(requested, self.capacity_bytes)
+
+    def init_state(self, num_qubits: int, precision=Precision.DOUBLE):
+        self._check_capacity(num_qubits, precision)
+        devs = self.shard_devices(num_qubits, precision)
+        if devs is not None:
+            from . import multidevice as md
+            st = md.init_sharded(self, num_qubits, precision, devs)
+            self.live_states += 1
+            return st
         t = self._alloc(num_qubits, precision)
         _native.check(_native.lib().svb_fill_basis(C.c_void_p(t.data_ptr()), num_qubits,
                                                    prec_code(precision), 0, C.c_void_p(self.stream())))
         self.live_states += 1
         return DeviceStateVector(num_qubits, precision, t, self)
 
-    def adopt(self, num_qubits: int, precision, amplitudes) -> DeviceStateVector:
+    def adopt(self, num_qubits: int, precision, amplitudes):
         p = as_precision(precision)
+        self._check_capacity(num_qubits, precision)
+        devs = None if isinstance(amplitudes, torch.Tensor) else self.shard_devices(num_qubits, precision)
+        if devs is not None:
+            from . import multidevice as md
+            host = np.ascontiguousarray(amplitudes, dtype=p.dtype).reshape(-1)
+            if host.size != 1 << num_qubits:
+                raise ValueError("amplitude count does not match num_qubits")
+            L = host.size // len(devs)
+            shards = [self.device_engine(d).adopt(num_qubits - (len(devs).bit_length() - 1), p,
+                                                  host[r * L:(r + 1) * L]) for r, d in enumerate(devs)]
+            self.live_states += 1
+            return md.ShardedDeviceState(self, num_qubits, p, shards, list(range(num_qubits)))
         if isinstance(amplitudes, torch.Tensor):
             t = amplitudes.to(self.device, _TORCH_DTYPE[p.value]).contiguous()
         else:
@@ -228,14 +299,22 @@ class B200Engine(EngineBase):
         return DeviceStateVector(num_qubits, precision, t, self)
 
     def release(self, state) -> None:
-        if isinstance(state, DeviceStateVector):
+        from .multidevice import ShardedDeviceState
+        if isinstance(state, ShardedDeviceState):
+            for sh in state.shards:
+                sh._engine.release(sh)
+            state.shards = []
+        elif isinstance(state, DeviceStateVector):
             state.tensor = None
         self.live_states -= 1
 
-    def apply_gate(self, state: DeviceStateVector, op):
+    def apply_gate(self, state, op):
         n = state.num_qubits
         if any(not 0 <= t < n for t in op.targets):
             raise ValueError(f"target out of range for {n} qubits: {op.targets}")
+        from .multidevice import ShardedDeviceState, apply_sharded
+        if isinstance(state, ShardedDeviceState):
+            return apply_sharded(state, [op])
         self._apply(state, effective_unitary(op), tuple(op.targets))
         return state
 
@@ -292,6 +371,16 @@ class B200Engine(EngineBase):
         for i, op in enumerate(circuit.gates):
             if any(not 0 <= t < circuit.num_qubits for t in op.targets):
                 raise ValueError(f"target out of range for {circuit.num_qubits} qubits: {op.targets}")
+        devs = self.shard_devices(circuit.num_qubits, precision)
+        if devs is not None and checkpoint is None and circuit.gates:
+            # too big for one device: sharded over the box's GPUs (the north
+            # star's replacement for ref memory.py:290-340's CPU fallback)
+            from . import multidevice as md
+            self._check_capacity(circuit.num_qubits, precision)
+            state = md.run_circuit_sharded(self, circuit, precision, devs)
+            self.live_states += 1
+            self.synchronize()
+            return state
         state = self.init_state(circuit.num_qubits, precision)
         if checkpoint is not None:
             for i, op in enumerate(circuit.gates):
@@ -303,7 +392,10 @@ class B200Engine(EngineBase):
         return state
 
     # ------------------------------------------------------- observables (K6)
-    def norm_squared(self, state: DeviceStateVector) -> float:
+    def norm_squared(self, state) -> float:
+        from .multidevice import ShardedDeviceState
+        if isinstance(state, ShardedDeviceState):
+            return state.norm_squared()
         out = C.c_double()
         _native.check(_native.lib().svb_norm2(C.c_void_p(state.tensor.data_ptr()), state.num_qubits,
                                               prec_code(state.precision), C.byref(out),
@@ -314,6 +406,14 @@ class B200Engine(EngineBase):
         """<a|b> accumulated in FP64 on the device."""
         if a.num_qubits != b.num_qubits:
             raise ValueError(f"qubit counts differ: {a.num_qubits} vs {b.num_qubits}")
+        from .multidevice import ShardedDeviceState, canonicalize
+        if isinstance(a, ShardedDeviceState) or isinstance(b, ShardedDeviceState):
+            if not (isinstance(a, ShardedDeviceState) and isinstance(b, ShardedDeviceState)) or \
+                    a.world != b.world:
+                raise ValueError("inner product of states sharded differently")
+            canonicalize(a)
+            canonicalize(b)
+            return sum(sa._engine.inner(sa, sb) for sa, sb in zip(a.shards, b.shards))
         # mixed precisions: both promoted to complex128 in the kernel (ref
         # engines.py:340-346), no copy of either state
         out = (C.c_double * 2)()
@@ -328,44 +428,75 @@ class B200Engine(EngineBase):
             ov /= self.norm_squared(a) * self.norm_squared(b)
         return float(ov)
 
-    def sample(self, state: DeviceStateVector, shots: int, seed: int):
+    def sample(self, state, shots: int, seed: int):
         """shots draws from |amp|^2 with the reference's semantics (ref
         engines.py:307-337): Philox(key=seed) uniforms scaled by the total,
-        inverse CDF (searchsorted side='right'), qubit 0 rightmost.  The CDF
-        never leaves the device; only the draws and the indices cross PCIe."""
+        inverse CDF (searchsorted side='right'), qubit 0 rightmost.  FP64 sums
+        of |amp|^2 over blocks of 4096 amplitudes are reduced on the device,
+        their prefix sums taken sequentially on the host (numpy cumsum, as the
+        reference does over the whole vector), and each draw is resolved
+        inside its block on the device: the amplitudes never leave HBM.
+        Sharded states (restored to the identity layout) are resolved shard by
+        shard."""
         from .engines import SampleResult
+        from .multidevice import ShardedDeviceState, canonicalize
         if shots < 0:
             raise ValueError("shots must be >= 0")
         if shots == 0:
             return SampleResult({}, 0)
         n = state.num_qubits
-        lb = min(n, 12)
-        nb = 1 << (n - lb)
-        dev = state.tensor.device
-        sums = torch.empty(nb, dtype=torch.float64, device=dev)
+        if isinstance(state, ShardedDeviceState):
+            canonicalize(state)
+            parts = list(state.shards)
+        else:
+            parts = [state]
+        nl = parts[0].num_qubits
+        lb = min(nl, 12)
+        nb = 1 << (nl - lb)
         pc = prec_code(state.precision)
-        s = C.c_void_p(self.stream())
-        _native.check(_native.lib().svb_block_sums(C.c_void_p(state.tensor.data_ptr()), n, pc, lb,
-                                                   C.c_void_p(sums.data_ptr()), s))
-        cum = torch.cumsum(sums, 0)
-        total = float(cum[-1].item())
+        sums = []
+        for sh in parts:
+            eng = sh._engine
+            dev_sums = torch.empty(nb, dtype=torch.float64, device=sh.tensor.device)
+            _native.check(_native.lib().svb_block_sums(C.c_void_p(sh.tensor.data_ptr()), nl, pc, lb,
+                                                       C.c_void_p(dev_sums.data_ptr()),
+                                                       C.c_void_p(eng.stream())))
+            sums.append(dev_sums.cpu().numpy())
+        cum = np.cumsum(np.concatenate(sums))
+        total = float(cum[-1])
         if abs(total - 1.0) > 1e-4:
             raise ValueError(f"state norm deviates from 1 by {abs(total - 1.0):.2e}; "
                              "refusing to sample from a corrupted state")
-        draws = np.random.Generator(np.random.Philox(key=seed)).random(shots)
-        x = torch.from_numpy(draws * total).to(dev)
-        idx = torch.empty(shots, dtype=torch.int64, device=dev)
-        _native.check(_native.lib().svb_sample_search(
-            C.c_void_p(state.tensor.data_ptr()), n, pc, lb, C.c_void_p(cum.data_ptr()),
-            C.c_void_p(x.data_ptr()), shots, C.c_void_p(idx.data_ptr()), s))
-        host = np.minimum(idx.cpu().numpy(), (1 << n) - 1)
+        draws = np.random.Generator(np.random.Philox(key=seed)).random(shots) * total
+        blk = np.minimum(np.searchsorted(cum, draws, side="right"), cum.size - 1)
+        owner = blk // nb
+        out = np.empty(shots, dtype=np.int64)
+        for r, sh in enumerate(parts):
+            sel = np.nonzero(owner == r)[0]
+            if sel.size == 0:
+                continue
+            eng = sh._engine
+            dev = sh.tensor.device
+            base = float(cum[r * nb - 1]) if r else 0.0  # the shard's blocks, relative
+            dcum = torch.from_numpy(np.ascontiguousarray(cum[r * nb:(r + 1) * nb] - base)).to(dev)
+            x = torch.from_numpy(np.ascontiguousarray(draws[sel] - base)).to(dev)
+            idx = torch.empty(sel.size, dtype=torch.int64, device=dev)
+            _native.check(_native.lib().svb_sample_search(
+                C.c_void_p(sh.tensor.data_ptr()), nl, pc, lb, C.c_void_p(dcum.data_ptr()),
+                C.c_void_p(x.data_ptr()), int(sel.size), C.c_void_p(idx.data_ptr()),
+                C.c_void_p(eng.stream())))
+            out[sel] = idx.cpu().numpy() + (r << nl)
+        host = np.minimum(out, (1 << n) - 1)
         values, counts = np.unique(host, return_counts=True)
         return SampleResult({format(int(v), f"0{n}b"): int(c) for v, c in zip(values, counts)}, shots)
 
-    def probabilities(self, state: DeviceStateVector, chunk_bytes: int = D2H_CHUNK_BYTES) -> np.ndarray:
+    def probabilities(self, state, chunk_bytes: int = D2H_CHUNK_BYTES) -> np.ndarray:
         """|amp|^2 in FP64 (ref circuit.py:203-205), computed on the device one
         chunk at a time into a reusable buffer and copied into the host array:
         no 2^n-double device array next to a near-HBM-sized state."""
+        from .multidevice import ShardedDeviceState
+        if isinstance(state, ShardedDeviceState):
+            return state.probabilities()
         n = 1 << state.num_qubits
         out = np.empty(n, dtype=np.float64)
         per = max(1, min(n, chunk_bytes // 8))

@@ -541,6 +541,7 @@ void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
 }
 
 // ------------------------------------------------------------ k_gemm_pass
+constexpr int kGemmDefaultWarps = 8;
 // A-operand word of each tile bit in a phase layout (register bits j0..j4 =
 // map[0..4], row bits m0..m6 = map[5..11]); word = m 32 + ((j >> 2) ^ (m & 7)) 4
 // + (j & 3), the K-major SWIZZLE_128B canonical layout of svb_gemmpass.cuh.
@@ -748,7 +749,7 @@ void gemm_layout(const int* prev_lanes, const int* R, const std::vector<int>& pr
 // bits before or after the GEMM they commute with, and choose every phase's
 // qubit order for conflict-free A writes and coalesced loads / stores.
 // Returns false (pass left unchanged) when the pass does not fit the kernel.
-bool build_gemm_pass(Pass& p, int streams) {
+bool build_gemm_pass(Pass& p, int streams, int warps) {
   const int T = kGemmTileBits;
   if (p.T != T) return false;
   for (const KernelOp& op : p.ops) {  // unitary ops only (the kernel rescales by the tile norm)
@@ -1022,6 +1023,7 @@ bool build_gemm_pass(Pass& p, int streams) {
   p.reg_bits = 5;
   p.thread_bits = 7;
   p.streams = streams >= 2 && streams <= 4 ? streams : 4;
+  p.gemm_warps = warps == 4 ? 4 : warps == 8 ? 8 : kGemmDefaultWarps;
   p.gemm = true;
   p.mma_phases = false;
   p.renorm = true;
@@ -1415,7 +1417,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     int n_dense = 0;
     for (const KernelOp& o : p.ops) n_dense += o.kind == OP_DENSE;
     const int min_dense = opt.tc_min_dense > 0 ? opt.tc_min_dense : 2;
-    if (use_gemm && p.T == kGemmTileBits && n_dense >= min_dense && build_gemm_pass(p, opt.streams)) {
+    if (use_gemm && p.T == kGemmTileBits && n_dense >= min_dense && build_gemm_pass(p, opt.streams, opt.gemm_warps)) {
       // k_gemm_pass (lowered above)
     } else if (use_mma && opt.streams != 1 && p.T == 12 && build_phases(p, 5, prec, 7)) {
       // 12-qubit tiles: warp groups with their own tile streams (k_reg_pass TB 7)

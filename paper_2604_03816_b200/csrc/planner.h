@@ -88,6 +88,7 @@ struct Pass {
   // k_gemm_pass (c64): phases[0] = load layout + ops before the first GEMM,
   // phases[f >= 1] = GEMM tc_mats[f - 1] then element-wise diagonal ops
   bool gemm = false;
+  int gemm_warps = 4;             // warps per tile stream (4: 32 amplitudes per thread, 8: 16)
   int bank_conflicts = 0;         // sum over A writes of log2(bank-conflict degree)
   std::vector<std::vector<cd>> tc_mats;  // fused phase matrices (2^RB x 2^RB, row-major)
   std::vector<RegPhase> phases;

@@ -27,6 +27,13 @@ using namespace svb;
 
 namespace {
 
+// Shared-window address where a kernel's dynamic shared memory starts (no
+// static shared memory here, like the tile-pass kernels).
+__global__ void k_smem_base(uint32_t* out) {
+  extern __shared__ unsigned char s_dyn[];
+  *out = smem_addr(s_dyn);
+}
+
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -49,6 +56,7 @@ struct DeviceFacts {
   int max_smem = 0;
   int ctas_per_sm_c64 = 0;
   int ctas_per_sm_c128 = 0;
+  uint32_t dyn_smem_base = 0;  // shared-window address of dynamic shared memory
   bool attrs_set = false;
   // reduction scratch (device partials + pinned host copy), allocated once:
   // stream-ordered cudaMallocAsync next to a 100+ GiB torch allocation was
@@ -76,14 +84,24 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
-                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4>,
-                         (const void*)k_gemm_pass<3>,          (const void*)k_gemm_pass<2>,
+                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4, 4>,
+                         (const void*)k_gemm_pass<3, 4>,       (const void*)k_gemm_pass<2, 4>,
+                         (const void*)k_gemm_pass<4, 8>,       (const void*)k_gemm_pass<3, 8>,
+                         (const void*)k_gemm_pass<2, 8>,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
                          (const void*)k_reg_pass<float2, 5, 7, 4>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
       SVB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    {  // where dynamic shared memory starts (k_gemm_pass aligns its tiles in that window)
+      uint32_t* d = nullptr;
+      SVB_CUDA(cudaMalloc(&d, sizeof(uint32_t)));
+      k_smem_base<<<1, 1, 1024>>>(d);
+      SVB_CUDA(cudaGetLastError());
+      SVB_CUDA(cudaMemcpy(&f.dyn_smem_base, d, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      cudaFree(d);
+    }
     f.attrs_set = true;
   }
   *out = &f;
@@ -138,7 +156,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
   a.h.thread_bits = p.phases.empty() ? 8 : p.thread_bits;
   a.h.streams = p.phases.empty() ? 1 : p.streams;
   a.h.renorm = p.renorm ? 1 : 0;
-  a.h.gemm = p.gemm ? 1 : 0;
+  a.h.gemm = p.gemm ? (p.gemm_warps == 8 ? 8 : 4) : 0;
   if (p.gemm) a.h.tc_count = int(p.tc_mats.size());
   a.h.tc_mats = nullptr;
   int off = 0;
@@ -276,12 +294,15 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     if (a.h.gemm) {
       if (a.h.tma_rank < 1) return fail(SVB_EUNSUPPORTED, "k_gemm_pass needs a tensor map");
       const int ng = a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
-      void (*gfn)(float2*, PassArgs<float2>) = ng == 2 ? k_gemm_pass<2> : ng == 3 ? k_gemm_pass<3> : k_gemm_pass<4>;
-      const size_t smem_g = gemm_smem_layout(a.h, ng).total;
+      const int wpg = a.h.gemm == 8 ? 8 : 4;  // warps per tile stream
+      void (*gfn)(float2*, PassArgs<float2>) =
+          wpg == 8 ? (ng == 2 ? k_gemm_pass<2, 8> : ng == 3 ? k_gemm_pass<3, 8> : k_gemm_pass<4, 8>)
+                   : (ng == 2 ? k_gemm_pass<2, 4> : ng == 3 ? k_gemm_pass<3, 4> : k_gemm_pass<4, 4>);
+      const size_t smem_g = gemm_smem_layout(a.h, ng, f->dyn_smem_base).total;
       if (smem_g > size_t(f->max_smem)) return fail(SVB_EUNSUPPORTED, "gemm pass exceeds shared memory");
       long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count);
       if (grid < 1) grid = 1;
-      gfn<<<(unsigned)grid, ng * 128, smem_g, stream>>>(reinterpret_cast<float2*>(amps),
+      gfn<<<(unsigned)grid, ng * wpg * 32, smem_g, stream>>>(reinterpret_cast<float2*>(amps),
                                                        reinterpret_cast<const PassArgs<float2>&>(a));
       SVB_CUDA(cudaGetLastError());
       return SVB_OK;

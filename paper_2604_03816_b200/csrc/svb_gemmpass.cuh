@@ -64,17 +64,21 @@ struct GemmTables {
 };
 
 struct GemmSmem {
-  size_t pool, dthr, dout, red, tabs, mats, tiles, total;
+  size_t pool, dthr, dout, red, orig, tabs, mats, tiles, total;
 };
-__host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng) {
+// `base` = shared-window address of the dynamic shared memory (the tile
+// buffers are placed 16 KB-aligned in that window so that an A word's byte
+// address is (buffer | offset): XOR-composable, no add per store)
+__host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng, uint32_t base) {
   GemmSmem l;
   l.pool = 128;  // barriers + TMEM slot
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(float2), 128);
   l.dout = l.dthr + align_up(size_t(h.n_ops) * 128, 128);
   l.red = l.dout + align_up(size_t(ng) * 2 * kMaxOps * sizeof(int), 128);
-  l.tabs = align_up(l.red + size_t(ng) * 8 * sizeof(float), 128);
+  l.orig = align_up(l.red + size_t(ng) * 16 * sizeof(float), 128);
+  l.tabs = align_up(l.orig + size_t(ng) * 2 * sizeof(long long), 128);
   l.mats = align_up(l.tabs + sizeof(GemmTables), 1024);
-  l.tiles = l.mats + size_t(h.tc_count) * kMmaMatBytes;
+  l.tiles = align_up(base + l.mats + size_t(h.tc_count) * kMmaMatBytes, 16384) - base;
   l.total = l.tiles + size_t(ng) * kGemmTileBytes;
   return l;
 }
@@ -95,11 +99,11 @@ __device__ __forceinline__ void t5_mma_ss(uint32_t d, uint64_t a, uint64_t b, ui
 
 // fp16 hi/lo split of a (scaled) complex amplitude, stored as the f16x2 words
 // of A_hi and A_lo (re in the low half: K index 2j, im: 2j + 1)
-__device__ __forceinline__ void gemm_split_store(uint32_t* __restrict__ A, uint32_t w, float xr, float xi) {
+__device__ __forceinline__ void gemm_split_store(uint32_t addr, float xr, float xi) {
   const uint32_t hh = pack_half2(xr, xi);
   const float2 hf = unpack_half2(hh);
-  A[w] = hh;
-  A[w + kGemmAWords] = pack_half2(xr - hf.x, xi - hf.y);
+  const uint32_t ll = pack_half2(xr - hf.x, xi - hf.y);
+  asm volatile("st.shared.b32 [%0], %1;\n st.shared.b32 [%0+16384], %2;" ::"r"(addr), "r"(hh), "r"(ll) : "memory");
 }
 
 // tcgen05.ld 16x256b, 8 repetitions: 16 TMEM lanes x 64 columns per warp;
@@ -124,22 +128,56 @@ __device__ __forceinline__ void t5_ld16x256_x8(uint32_t taddr, uint32_t (&d)[32]
 //    which lets the planner put low tile qubits there (coalesced stores,
 //    conflict-free A writes).
 template <bool LD16>
-__device__ __forceinline__ void gemm_read_half(uint32_t dcol, int half, float2 (&u)[16]) {
-  uint32_t d[32];
-  if constexpr (!LD16) {
+__device__ __forceinline__ void gemm_ld_issue(uint32_t dcol, int half, uint32_t (&d)[32]) {
+  if constexpr (!LD16)
     t5_ld32(dcol + 32u * half, d);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  else
+    t5_ld16x256_x8(dcol + (uint32_t(16 * half) << 16), d);
+}
+
+// tcgen05.wait::ld with the loaded registers tied to it, so no consumer can be
+// scheduled before the wait
+__device__ __forceinline__ void t5_wait_ld_tied(uint32_t (&d)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]), "+r"(d[6]), "+r"(d[7]),
+                 "+r"(d[8]), "+r"(d[9]), "+r"(d[10]), "+r"(d[11]), "+r"(d[12]), "+r"(d[13]), "+r"(d[14]),
+                 "+r"(d[15]), "+r"(d[16]), "+r"(d[17]), "+r"(d[18]), "+r"(d[19]), "+r"(d[20]), "+r"(d[21]),
+                 "+r"(d[22]), "+r"(d[23]), "+r"(d[24]), "+r"(d[25]), "+r"(d[26]), "+r"(d[27]), "+r"(d[28]),
+                 "+r"(d[29]), "+r"(d[30]), "+r"(d[31])
+               :
+               : "memory");
+}
+
+// Registers of one half in the phase's thread layout:
+//  * 32x32b (thread = row m; register index = column j): columns 32 half ..;
+//  * 16x256b (PH_LD16): register index = j2 j3 j4 | row bit 3 | row bit 4 =
+//    half; lanes = j0 j1 | row bits 0..2 -- two column bits on the lanes,
+//    which lets the planner put low tile qubits there (coalesced stores,
+//    conflict-free A writes).
+template <bool LD16>
+__device__ __forceinline__ void gemm_unpack(const uint32_t (&d)[32], float2 (&u)[16]) {
+  if constexpr (!LD16) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) u[q] = make_float2(__uint_as_float(d[2 * q]), __uint_as_float(d[2 * q + 1]));
   } else {
-    t5_ld16x256_x8(dcol + (uint32_t(16 * half) << 16), d);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int c = 0; c < 8; ++c)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh)
         u[c | hh << 3] = make_float2(__uint_as_float(d[4 * c + 2 * hh]), __uint_as_float(d[4 * c + 2 * hh + 1]));
   }
+}
+
+// Both halves of this thread's D row: two loads in flight, one wait.
+template <bool LD16>
+__device__ __forceinline__ void gemm_read_row(uint32_t dcol, float2 (&u0)[16], float2 (&u1)[16]) {
+  uint32_t d0[32], d1[32];
+  gemm_ld_issue<LD16>(dcol, 0, d0);
+  gemm_ld_issue<LD16>(dcol, 1, d1);
+  t5_wait_ld_tied(d0);
+  t5_wait_ld_tied(d1);
+  gemm_unpack<LD16>(d0, u0);
+  gemm_unpack<LD16>(d1, u1);
 }
 
 // Diagonal op on one half: one table factor per amplitude (table index =
@@ -152,10 +190,11 @@ __device__ __forceinline__ void gemm_diag_half(float2 (&u)[16], const OpDesc& op
   for (int q = 0; q < 16; ++q) u[q] = cmul(u[q], table[dbase | rmap[q | half << 4]]);
 }
 
-// Convert one half into the A operand of the next GEMM: word of register rho
-// = wbase ^ XOR of wr[bit] over rho's bits, visited in Gray-code order.
-__device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const float2 (&u)[16], uint32_t wbase,
-                                                const uint32_t* __restrict__ wr, int half) {
+// Convert one half into the A operand of the next GEMM: the shared address of
+// register rho = wbase ^ XOR of wr[bit] (byte offsets) over rho's bits,
+// visited in Gray-code order -- one LOP3 per amplitude.
+__device__ __forceinline__ void gemm_write_half(const float2 (&u)[16], uint32_t wbase, const uint32_t* __restrict__ wr,
+                                                int half) {
   uint32_t basis[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) basis[i] = wr[i];
@@ -164,61 +203,88 @@ __device__ __forceinline__ void gemm_write_half(uint32_t* __restrict__ A, const 
   for (int i = 0; i < 16; ++i) {
     if (i) w ^= basis[ctz_c(i)];
     const int r = i ^ (i >> 1);
-    gemm_split_store(A, w, u[r].x, u[r].y);
+    gemm_split_store(w, u[r].x, u[r].y);
   }
 }
 
 // One tile's GEMM-phase epilogue with a compile-time read-out shape: D ->
 // registers -> diagonal ops -> hi/lo A words of the next GEMM.
-template <bool LD16>
-__device__ __forceinline__ void gemm_phase_body(uint32_t* __restrict__ A, uint32_t dcol, const PassArgs<float2>& args,
-                                                const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
-                                                const int* dslot, int gt, uint32_t wbase, const uint32_t* wr) {
-  constexpr int NTG = 128;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    float2 u[16];
-    gemm_read_half<LD16>(dcol, half, u);
-    for (int o = ph.op_begin; o < ph.op_end; ++o)
-      gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
-                     int(dthr[o * NTG + gt]) | (args.h.has_outside ? dslot[o] : 0), half);
-    gemm_write_half(A, u, wbase, wr, half);
+// The halves a thread owns: both (4 warps per tile stream) or the one its
+// warp index selects (8 warps: register bit 4 becomes a warp bit).
+template <int NH, bool LD16>
+__device__ __forceinline__ void gemm_read_owned(uint32_t dcol, int h0, float2 (&u)[NH][16]) {
+  if constexpr (NH == 2) {
+    gemm_read_row<LD16>(dcol, u[0], u[1]);
+  } else {
+    uint32_t d[32];
+    gemm_ld_issue<LD16>(dcol, h0, d);
+    t5_wait_ld_tied(d);
+    gemm_unpack<LD16>(d, u[0]);
   }
 }
 
-template <bool LD16>
-__device__ __forceinline__ float gemm_norm_body(uint32_t dcol) {
+template <int NH, bool LD16>
+__device__ __forceinline__ void gemm_phase_body(uint32_t dcol, const PassArgs<float2>& args,
+                                                const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
+                                                const int* dslot, int gt7, int h0, uint32_t wbase,
+                                                const uint32_t* wr) {
+  float2 u[NH][16];
+  gemm_read_owned<NH, LD16>(dcol, h0, u);
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    const int half = h0 + k;
+    for (int o = ph.op_begin; o < ph.op_end; ++o)
+      gemm_diag_half(u[k], args.ops[o], pool + args.ops[o].coeff_off,
+                     int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
+    gemm_write_half(u[k], wbase, wr, half);
+  }
+}
+
+// sum of |amp|^2 with 8 independent FMA chains (one chain would serialise
+// 64 dependent FMAs)
+template <int N>
+__device__ __forceinline__ float norm2_chains(const float2 (&u)[N]) {
+  float acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+#pragma unroll
+  for (int q = 0; q < N; ++q) acc[q & 7] = fmaf(u[q].x, u[q].x, fmaf(u[q].y, u[q].y, acc[q & 7]));
+  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
+template <int NH, bool LD16>
+__device__ __forceinline__ float gemm_norm_body(uint32_t dcol, int h0) {
+  float2 u[NH][16];
+  gemm_read_owned<NH, LD16>(dcol, h0, u);
   float w = 0.f;
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    float2 u[16];
-    gemm_read_half<LD16>(dcol, half, u);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) w = fmaf(u[q].x, u[q].x, fmaf(u[q].y, u[q].y, w));
-  }
+  for (int k = 0; k < NH; ++k) w += norm2_chains(u[k]);
   return w;
 }
 
 // Final store of one tile (last layout): diagonal ops, undo the scale /
 // restore the norm (factor f), 16-byte stores when register bit 0 is tile
 // bit 0 (`pairs`), else 8-byte.
-template <bool LD16>
+// OFF: int when every offset of the tile fits 31 bits (n_local <= 31: one
+// IADD per store instead of a 64-bit add), else long long.
+template <int NH, bool LD16, class OFF>
 __device__ __forceinline__ void gemm_store_body(float2* __restrict__ dst, uint32_t dcol, const PassArgs<float2>& args,
                                                 const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
-                                                const int* dslot, int gt, const long long* __restrict__ sr,
+                                                const int* dslot, int gt7, int h0, const long long* __restrict__ sr,
                                                 float f, bool pairs) {
-  constexpr int NTG = 128;
+  float2 uu[NH][16];
+  gemm_read_owned<NH, LD16>(dcol, h0, uu);
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    float2 u[16];
-    gemm_read_half<LD16>(dcol, half, u);
+  for (int k = 0; k < NH; ++k) {
+    const int half = h0 + k;
+    float2 (&u)[16] = uu[k];
     for (int o = ph.op_begin; o < ph.op_end; ++o)
       gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
-                     int(dthr[o * NTG + gt]) | (args.h.has_outside ? dslot[o] : 0), half);
-    long long goff[4];
+                     int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
+    OFF goff[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) goff[i] = sr[i];
-    long long o = half ? sr[4] : 0;
+    for (int i = 0; i < 4; ++i) goff[i] = OFF(sr[i]);
+    OFF o = half ? OFF(sr[4]) : OFF(0);
     if (pairs) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -253,8 +319,8 @@ __device__ __forceinline__ void gemm_tables(GemmTables& t, const PassArgs<float2
     uint32_t w = 0;
     for (int b = 0; b < 7; ++b)
       if ((gt >> b) & 1) w ^= wt[cur.map[5 + b]];
-    t.wb[p][gt] = w;
-    if (gt < 5) t.wr[p][gt] = wt[cur.map[gt]];
+    t.wb[p][gt] = 4 * w;  // byte offsets within A_hi
+    if (gt < 5) t.wr[p][gt] = 4u * wt[cur.map[gt]];
   }
   const PhaseDesc& p0 = args.phases[0];
   uint32_t x = 0;
@@ -269,26 +335,33 @@ __device__ __forceinline__ void gemm_tables(GemmTables& t, const PassArgs<float2
   if (gt < 5) t.str[gt] = 1LL << gpos(pl.map[gt], h);
 }
 
-template <int NG>
-__global__ void __launch_bounds__(NG * 128, 1)
+// NG tile streams of WPG warps: WPG 4 -> a thread holds 32 amplitudes (both
+// register halves); WPG 8 -> 16 (register bit 4 is warp bit 2 of the stream),
+// twice the warps per scheduler to hide the GEMM / TMEM / barrier latency.
+template <int NG, int WPG = 4>
+__global__ void __launch_bounds__(NG * WPG * 32, 1)
     k_gemm_pass(float2* __restrict__ amps, const __grid_constant__ PassArgs<float2> args) {
-  constexpr int NTG = 128;
+  constexpr int NTG = WPG * 32;
+  constexpr int NH = WPG == 8 ? 1 : 2;  // register halves per thread
   constexpr int T = kGemmT;
   constexpr uint32_t kTmemCols = NG > 2 ? 256 : 128;
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
-  const GemmSmem lay = gemm_smem_layout(h, NG);
+  const GemmSmem lay = gemm_smem_layout(h, NG, smem_addr(smem));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [group] tile landed
   uint64_t* mbar = full + NG;                           // [group] GEMM committed
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + NG);
   float2* pool = reinterpret_cast<float2*>(smem + lay.pool);
   unsigned char* dthr = smem + lay.dthr;                 // [op][thread] diagonal index, thread part
   int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [group][2][op] outside-tile part
-  float* red = reinterpret_cast<float*>(smem + lay.red);  // [group][in 4 | out 4] norm partials
+  float* red = reinterpret_cast<float*>(smem + lay.red);  // [group][in 8 | out 8] norm partials
+  long long* orig = reinterpret_cast<long long*>(smem + lay.orig);  // [group][2] tile origins
   const uint32_t mats = smem_addr(smem + lay.mats);
   unsigned char* tiles = smem + lay.tiles;
   const int tid = threadIdx.x;
   const int group = tid / NTG, gt = tid % NTG, wig = gt >> 5, lane = tid & 31;
+  const int gt7 = gt & 127;                 // the thread's 7 row bits (lane + warp quarter)
+  const int h0 = NH == 2 ? 0 : gt >> 7;     // first register half owned
   const int P = h.n_phases - 1;  // GEMM phases
 
   if (tid == 0) {
@@ -310,30 +383,33 @@ __global__ void __launch_bounds__(NG * 128, 1)
     uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);
     for (int e = tid; e < h.tc_count * (kMmaMatBytes / 16); e += NG * NTG) dst[e] = src[e];
   }
-  for (int e = tid; e < h.n_ops * NTG; e += NG * NTG) {
-    const OpDesc& op = args.ops[e / NTG];
-    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % NTG) : 0;
+  for (int e = tid; e < h.n_ops * 128; e += NG * NTG) {
+    const OpDesc& op = args.ops[e / 128];
+    dthr[e] = op.kind == OP_DIAG ? (unsigned char)diag_thread_part(op, e % 128) : 0;
   }
   GemmTables& tab = *reinterpret_cast<GemmTables*>(smem + lay.tabs);
-  if (tid < NTG) gemm_tables(tab, args, tid);
+  if (tid < 128) gemm_tables(tab, args, tid);
   fence_proxy_async_smem();  // B operands written by the generic proxy, read by the tensor core
   t5_fence_before();
   __syncthreads();
   t5_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t dcol = tbase + uint32_t(group) * 64u + (uint32_t(wig * 32) << 16);  // this warp's D lanes
+  const uint32_t dcol = tbase + uint32_t(group) * 64u + (uint32_t((wig & 3) * 32) << 16);  // this warp's D lanes
 
   const int n_tiles = int(h.n_tiles);
   const int mine = int(blockIdx.x) < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
   float2* buf = reinterpret_cast<float2*>(tiles + size_t(group) * kGemmTileBytes);
-  uint32_t* A = reinterpret_cast<uint32_t*>(buf);
-  const uint32_t abase = smem_addr(buf);
+  const uint32_t abase = smem_addr(buf);  // 16 KB aligned (gemm_smem_layout)
+  if (abase & 16383u) __trap();          // host and device disagree on the shared window
+  // every shard offset of a tile fits 31 bits (int store offsets)
+  const bool small = (h.m == 0 ? h.L : h.high_sorted[h.m - 1] + 1) <= 31;
 
   // the stream's tile load (warp 0 of the group: lane 0 issues the TMA, all
-  // lanes publish the outside-tile diagonal index parts of the tile)
+  // lanes publish the tile origin and the outside-tile diagonal index parts)
   auto load = [&](int it, int xs) {
     const int tile = int(blockIdx.x) + it * int(gridDim.x);
     const long long tb = tile_base(tile, h);
+    if (lane == 0) orig[group * 2 + xs] = tb;  // published with the tile (mbarrier release)
     if (h.has_outside) {
       int* slot = dout + (group * 2 + xs) * kMaxOps;
       for (int i = lane; i < h.n_ops; i += 32)
@@ -357,67 +433,78 @@ __global__ void __launch_bounds__(NG * 128, 1)
     }
     __syncwarp();
   };
+  auto sum_red = [&](int off) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPG; ++w) s += red[group * 16 + off + w];
+    return s;
+  };
 
   uint32_t fpar = 0, mpar = 0;
   int xs = 0;
   if (wig == 0 && group < mine) load(group, 0);
   for (int it = group; it < mine; it += NG, xs ^= 1) {
-    const int tile = int(blockIdx.x) + it * int(gridDim.x);
-    const long long origin = tile_base(tile, h);
     const int* dslot = dout + (group * 2 + xs) * kMaxOps;
     mbar_wait(&full[group], fpar);
     fpar ^= 1;
+    const long long origin = orig[group * 2 + xs];
 
     // ---- phase 0: linear tile -> registers (load layout), tile norm, scale,
     // ops_0, A of GEMM 1 written in place
     float S, n2in;
     {
-      float2 v[32];
+      float2 v[NH][16];
       const PhaseDesc& p0 = args.phases[0];
-      uint32_t x = tab.ld[gt];
-      if (p0.map[0] == 0) {
-        // register bit 0 = tile bit 0: adjacent pairs, 16-byte loads
-        uint32_t basis[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) basis[i] = tab.ldr[1 + i];
+      for (int k = 0; k < NH; ++k) {
+        uint32_t x = tab.ld[gt7] ^ ((h0 + k) ? tab.ldr[4] : 0u);
+        if (p0.map[0] == 0) {
+          // register bit 0 = tile bit 0: adjacent pairs, 16-byte loads
+          uint32_t basis[3];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i) x ^= basis[ctz_c(i)];
-          const float4 q = *reinterpret_cast<const float4*>(buf + x);
-          const int r = (i ^ (i >> 1)) << 1;
-          v[r] = make_float2(q.x, q.y);
-          v[r | 1] = make_float2(q.z, q.w);
-        }
-      } else {
-        uint32_t basis[5];
+          for (int i = 0; i < 3; ++i) basis[i] = tab.ldr[1 + i];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) basis[i] = tab.ldr[i];
+          for (int i = 0; i < 8; ++i) {
+            if (i) x ^= basis[ctz_c(i)];
+            const float4 q = *reinterpret_cast<const float4*>(buf + x);
+            const int r = (i ^ (i >> 1)) << 1;
+            v[k][r] = make_float2(q.x, q.y);
+            v[k][r | 1] = make_float2(q.z, q.w);
+          }
+        } else {
+          uint32_t basis[4];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i) x ^= basis[ctz_c(i)];
-          v[i ^ (i >> 1)] = buf[x];
+          for (int i = 0; i < 4; ++i) basis[i] = tab.ldr[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i) x ^= basis[ctz_c(i)];
+            v[k][i ^ (i >> 1)] = buf[x];
+          }
         }
       }
       {
-        const float w = warp_norm2(v);
-        if (lane == 0) red[group * 8 + wig] = w;
+        float w = 0.f;
+#pragma unroll
+        for (int k = 0; k < NH; ++k) w += norm2_chains(v[k]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0) red[group * 16 + wig] = w;
       }
       group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
-      n2in = red[group * 8] + red[group * 8 + 1] + red[group * 8 + 2] + red[group * 8 + 3];
+      n2in = sum_red(0);
       // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
       const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
       const int se = min(max(268 - ebits, 1), 253);
       S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
-      const uint32_t wb0 = tab.wb[0][gt];
+      const uint32_t wb0 = tab.wb[0][gt7];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float2 u[16];
+      for (int k = 0; k < NH; ++k) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) u[q] = make_float2(v[q | half << 4].x * S, v[q | half << 4].y * S);
+        for (int q = 0; q < 16; ++q) v[k][q] = make_float2(v[k][q].x * S, v[k][q].y * S);
         for (int o = p0.op_begin; o < p0.op_end; ++o)
-          gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
-                         int(dthr[o * NTG + gt]) | (h.has_outside ? dslot[o] : 0), half);
-        gemm_write_half(A, u, wb0, tab.wr[0], half);
+          gemm_diag_half(v[k], args.ops[o], pool + args.ops[o].coeff_off,
+                         int(dthr[o * 128 + gt7]) | (h.has_outside ? dslot[o] : 0), h0 + k);
+        gemm_write_half(v[k], abase | wb0, tab.wr[0], h0 + k);
       }
     }
     fence_proxy_async_smem();
@@ -446,10 +533,11 @@ __global__ void __launch_bounds__(NG * 128, 1)
       mpar ^= 1;
       t5_fence_after();
       if (p < P) {
+        const uint32_t wb = abase | tab.wb[p][gt7];
         if (ld16)
-          gemm_phase_body<true>(A, dcol, args, ph, pool, dthr, dslot, gt, tab.wb[p][gt], tab.wr[p]);
+          gemm_phase_body<NH, true>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         else
-          gemm_phase_body<false>(A, dcol, args, ph, pool, dthr, dslot, gt, tab.wb[p][gt], tab.wr[p]);
+          gemm_phase_body<NH, false>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         fence_proxy_async_smem();
         t5_fence_before();
         group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
@@ -460,21 +548,28 @@ __global__ void __launch_bounds__(NG * 128, 1)
       if (wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
       // tile 2-norm of the result (diagonal ops are unimodular: applied after)
       {
-        float w = ld16 ? gemm_norm_body<true>(dcol) : gemm_norm_body<false>(dcol);
+        float w = ld16 ? gemm_norm_body<NH, true>(dcol, h0) : gemm_norm_body<NH, false>(dcol, h0);
 #pragma unroll
         for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        if (lane == 0) red[group * 8 + 4 + wig] = w;
+        if (lane == 0) red[group * 16 + 8 + wig] = w;
       }
       group_bar<NG, NTG>(group);
-      const float n2out = red[group * 8 + 4] + red[group * 8 + 5] + red[group * 8 + 6] + red[group * 8 + 7];
+      const float n2out = sum_red(8);
       // undo the scale, restore the tile 2-norm (all ops unitary)
       const float f = n2out > 0.f ? sqrtf(n2in * S * S / n2out) / S : 1.f / S;
-      float2* __restrict__ dst = amps + origin + tab.st[gt];
+      float2* __restrict__ dst = amps + origin + tab.st[gt7];
       const bool pairs = ph.map[0] == 0;  // register bit 0 = tile bit 0: 16-byte stores
-      if (ld16)
-        gemm_store_body<true>(dst, dcol, args, ph, pool, dthr, dslot, gt, tab.str, f, pairs);
-      else
-        gemm_store_body<false>(dst, dcol, args, ph, pool, dthr, dslot, gt, tab.str, f, pairs);
+      if (small) {
+        if (ld16)
+          gemm_store_body<NH, true, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+        else
+          gemm_store_body<NH, false, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+      } else {
+        if (ld16)
+          gemm_store_body<NH, true, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+        else
+          gemm_store_body<NH, false, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+      }
       t5_fence_before();
     }
   }
