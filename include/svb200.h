@@ -70,7 +70,7 @@ typedef struct svb_plan_options {
                            groups of 128 threads (7 thread bits; 3-4 without a
                            producer warp), 1 = one stream of 256; 0 = default
                            (4 for c64 tensor-core phases, 3 for c128)           */
-  int gemm_warps;       /* k_gemm_pass warps per tile stream: 4 or 8 (0: default 8) */
+  int gemm_warps;       /* k_gemm_pass warps per tile stream: 4 or 8 (0: default 4) */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */
@@ -98,6 +98,10 @@ enum {
 };
 
 int svb_abi_version(void);
+/* Profiling aid: stage timestamps (clock64) of the last k_gemm_pass launch
+   (CTA 0, tile stream 0, first 8 tiles x 16 events) when the process runs
+   with SVB_GEMM_TRACE set; returns the number of entries copied (0: off). */
+int svb_debug_trace(unsigned long long* out, int n);
 const char* svb_last_error(void);
 
 /* Device facts (needs a GPU). */

@@ -20,7 +20,7 @@ ABI_VERSION = 1
 
 # every symbol declared in include/svb200.h (tests check the library exports them)
 EXPORTS = (
-    "svb_abi_version", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
+    "svb_abi_version", "svb_debug_trace", "svb_last_error", "svb_device_sm_count", "svb_fill_basis",
     "svb_apply_gate", "svb_plan_create", "svb_plan_num_passes", "svb_plan_pass_info",
     "svb_plan_pass_gates", "svb_plan_kernel_op", "svb_plan_phase", "svb_plan_phase_op",
     "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext", "svb_plan_phase_map",
@@ -72,6 +72,7 @@ def lib():
     ip, dp = C.POINTER(C.c_int), C.POINTER(C.c_double)
     sig = {
         "svb_abi_version": (i, []),
+        "svb_debug_trace": (i, [C.POINTER(C.c_ulonglong), i]),
         "svb_last_error": (C.c_char_p, []),
         "svb_device_sm_count": (i, [ip]),
         "svb_fill_basis": (i, [vp, i, i, ll, vp]),

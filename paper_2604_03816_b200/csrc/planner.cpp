@@ -541,7 +541,7 @@ void fuse_mma_phases(Pass& p, int min_dense, int max_mma, int prec) {
 }
 
 // ------------------------------------------------------------ k_gemm_pass
-constexpr int kGemmDefaultWarps = 8;
+constexpr int kGemmDefaultWarps = 4;  // measured: 8 warps (64 registers, spills) 17.4 vs 16.0 ms
 // A-operand word of each tile bit in a phase layout (register bits j0..j4 =
 // map[0..4], row bits m0..m6 = map[5..11]); word = m 32 + ((j >> 2) ^ (m & 7)) 4
 // + (j & 3), the K-major SWIZZLE_128B canonical layout of svb_gemmpass.cuh.
@@ -578,16 +578,15 @@ int gf2_rank(std::vector<int> v) {
 int smem_excess(const std::vector<long long>& addr, int bytes) {
   const int per = 128 / bytes;
   int total = 0;
+  long long words[128];
   for (int g0 = 0; g0 < 32; g0 += per) {
-    std::vector<std::vector<long long>> bank(32);
+    int nw = 0;
     for (int l = g0; l < g0 + per; ++l)
-      for (int w = 0; w < bytes / 4; ++w) {
-        const long long word = addr[l] / 4 + w;
-        auto& v = bank[word % 32];
-        if (std::find(v.begin(), v.end(), word) == v.end()) v.push_back(word);
-      }
-    int mx = 0;
-    for (auto& v : bank) mx = std::max(mx, int(v.size()));
+      for (int w = 0; w < bytes / 4; ++w) words[nw++] = addr[l] / 4 + w;
+    std::sort(words, words + nw);
+    nw = int(std::unique(words, words + nw) - words);
+    int cnt[32] = {0}, mx = 0;
+    for (int i = 0; i < nw; ++i) mx = std::max(mx, ++cnt[words[i] & 31]);
     total += mx;
   }
   const int ideal = 32 * bytes / 128;
@@ -634,16 +633,17 @@ int gemm_load_conflict(const int* map0) {
 // below L are contiguous; anything above lands in another segment)
 int gemm_store_cost(const int* map, int L) {
   const int bytes = map[0] == 0 ? 16 : 8;
-  std::vector<long long> seg;
+  long long seg[32];
   for (int l = 0; l < 32; ++l) {
     const long long x = lane_elem(map, l, 0);
     const long long lo = x & ((1LL << L) - 1), hi = x >> L;
-    const long long key = (hi << 40) | ((8 * lo) / 128);
-    if (std::find(seg.begin(), seg.end(), key) == seg.end()) seg.push_back(key);
+    seg[l] = (hi << 40) | ((8 * lo) / 128);
   }
+  std::sort(seg, seg + 32);
+  const int ns = int(std::unique(seg, seg + 32) - seg);
   const int ideal = 32 * bytes / 128;
   int lg = 0;
-  while ((ideal << lg) < int(seg.size())) ++lg;
+  while ((ideal << lg) < ns) ++lg;
   return lg;
 }
 
@@ -886,7 +886,9 @@ bool build_gemm_pass(Pass& p, int streams, int warps) {
   int best_cost = 1 << 30;
   std::vector<std::vector<int>> best_maps, best_alay;
   std::vector<int> best_ld16;
-  const int n_shape = P <= 3 ? (1 << P) : 2;
+  // read-out shape choices: the last phase's (store coalescing) always, the
+  // intermediate ones only for short passes (planning time)
+  const int n_shape = P <= 2 ? (1 << P) : 2;
   for (int a = 0; a < T; ++a)
     for (int b = a + 1; b < T; ++b) {
       if (a <= 3 || b <= 3) continue;  // lanes = {1, 2, 3, a, b}
@@ -1437,7 +1439,7 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       // FP64 work)
       // three producer-free streams by default (measured layered-30 332 ms vs
       // 379 ms with two, qft-30 121 vs 131 ms)
-      p.streams = opt.streams == 2 ? 2 : 3;
+      p.streams = opt.streams == 2 ? 2 : opt.streams == 4 ? 4 : 3;
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile

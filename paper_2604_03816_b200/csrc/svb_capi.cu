@@ -10,8 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -35,6 +37,7 @@ __global__ void k_smem_base(uint32_t* out) {
 }
 
 thread_local std::string g_err;
+unsigned long long* g_trace = nullptr;  // SVB_GEMM_TRACE buffer (managed memory)
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -84,12 +87,12 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_tile_pass<float2, 6>,  (const void*)k_tile_pass<double2, 2>,
                          (const void*)k_tile_pass<double2, 3>, (const void*)k_tile_pass<double2, 6>,
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
-                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4, 4>,
-                         (const void*)k_gemm_pass<3, 4>,       (const void*)k_gemm_pass<2, 4>,
-                         (const void*)k_gemm_pass<4, 8>,       (const void*)k_gemm_pass<3, 8>,
-                         (const void*)k_gemm_pass<2, 8>,
+                         (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4, 4, true>,
+                         (const void*)k_gemm_pass<4, 4, false>, (const void*)k_gemm_pass<3, 4, true>,
+                         (const void*)k_gemm_pass<2, 4, true>, (const void*)k_gemm_pass<4, 8, true>,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
+                         (const void*)k_reg_pass<double2, 4, 7, 4>,
                          (const void*)k_reg_pass<float2, 5, 7, 4>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
@@ -239,8 +242,12 @@ struct svb_plan {
   // execute_range writes the launch-time fields (tensor map of the state, TMA
   // ring depth) into the cached parameter blocks: one launcher at a time
   std::mutex mu;
+  // k_gemm_pass norm accumulators (2 doubles per pass), per (device, stream)
+  std::map<std::pair<int, cudaStream_t>, double*> normacc;
+
   ~svb_plan() {
     if (tc_dev) cudaFree(tc_dev);
+    for (auto& kv : normacc) cudaFree(kv.second);
   }
 };
 
@@ -293,11 +300,28 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   if constexpr (sizeof(C) == 8) {
     if (a.h.gemm) {
       if (a.h.tma_rank < 1) return fail(SVB_EUNSUPPORTED, "k_gemm_pass needs a tensor map");
-      const int ng = a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
+      static const int dbg = [] {
+        const char* e = std::getenv("SVB_GEMM_DEBUG");
+        return e ? std::atoi(e) : 0;
+      }();
+      a.h.debug = dbg;
+      static unsigned long long* trace = [] {
+        unsigned long long* t = nullptr;
+        if (std::getenv("SVB_GEMM_TRACE") && cudaMallocManaged(&t, 128 * sizeof(unsigned long long)) == cudaSuccess)
+          std::memset(t, 0, 128 * sizeof(unsigned long long));
+        return t;
+      }();
+      a.h.trace = trace;
+      g_trace = trace;
       const int wpg = a.h.gemm == 8 ? 8 : 4;  // warps per tile stream
+      const int ng = wpg == 8 ? 4 : a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
+      // SVB_GEMM_DEBUG bit 256: the 8-MMA (N = 128 hi product) variant, for comparison
+      // (measured slower: 17.1 vs 16.2 ms, the doubled TMEM read-out costs more)
       void (*gfn)(float2*, PassArgs<float2>) =
-          wpg == 8 ? (ng == 2 ? k_gemm_pass<2, 8> : ng == 3 ? k_gemm_pass<3, 8> : k_gemm_pass<4, 8>)
-                   : (ng == 2 ? k_gemm_pass<2, 4> : ng == 3 ? k_gemm_pass<3, 4> : k_gemm_pass<4, 4>);
+          wpg == 8 ? k_gemm_pass<4, 8, true>
+          : ng == 2 ? k_gemm_pass<2, 4, true>
+          : ng == 3 ? k_gemm_pass<3, 4, true>
+          : (dbg & 256) ? k_gemm_pass<4, 4, true> : k_gemm_pass<4, 4, false>;
       const size_t smem_g = gemm_smem_layout(a.h, ng, f->dyn_smem_base).total;
       if (smem_g > size_t(f->max_smem)) return fail(SVB_EUNSUPPORTED, "gemm pass exceeds shared memory");
       long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count);
@@ -321,7 +345,9 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     } else {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 4 || (a.h.thread_bits == 7 && a.h.reg_bits != 4))
         return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4 (two streams: 4)");
-      fn = a.h.thread_bits == 7 ? (a.h.streams == 3 ? k_reg_pass<C, 4, 7, 3> : k_reg_pass<C, 4, 7>)
+      fn = a.h.thread_bits == 7 ? (a.h.streams == 4   ? k_reg_pass<C, 4, 7, 4>
+                                   : a.h.streams == 3 ? k_reg_pass<C, 4, 7, 3>
+                                                      : k_reg_pass<C, 4, 7>)
            : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
                                 : k_reg_pass<C, 3>;
     }
@@ -475,7 +501,24 @@ template <class C>
 int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int first, int count, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(p->mu);
   if (int rc = upload_tc(p)) return rc;
+  double* acc = nullptr;
+  if constexpr (sizeof(C) == 8) {
+    bool any = false;
+    for (const Pass& ps : p->plan.passes) any = any || ps.gemm;
+    if (any) {
+      int dev = 0;
+      SVB_CUDA(cudaGetDevice(&dev));
+      double*& buf = p->normacc[{dev, s}];
+      if (!buf) SVB_CUDA(cudaMalloc(&buf, sizeof(double) * 2 * p->plan.passes.size()));
+      acc = buf;
+      // a new execution starts from pass 0: fresh accumulators (a range that
+      // continues an execution keeps the earlier passes' sums)
+      if (first == 0) SVB_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * 2 * p->plan.passes.size(), s));
+    }
+  }
   for (int i = first; i < first + count; ++i) {
+    args[i].h.normacc = acc;
+    args[i].h.pass_index = i;
     int rc = launch_pass<C>(args[i], p->plan.n, static_cast<C*>(amps), s);
     if (rc) return rc;
   }
@@ -521,6 +564,15 @@ int dot_impl(const void* a, const void* b, long long n, double* out2, cudaStream
 extern "C" {
 
 int svb_abi_version(void) { return SVB_ABI_VERSION; }
+
+int svb_debug_trace(unsigned long long* out, int n) {
+  if (!out || n < 0) return fail(SVB_EINVAL, "bad argument");
+  if (!g_trace) return 0;
+  cudaDeviceSynchronize();
+  const int m = std::min(n, 128);
+  std::memcpy(out, g_trace, sizeof(unsigned long long) * m);
+  return m;
+}
 
 const char* svb_last_error(void) { return g_err.c_str(); }
 

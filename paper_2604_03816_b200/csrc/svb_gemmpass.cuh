@@ -89,12 +89,32 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-__device__ __forceinline__ void t5_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+// instruction descriptor: D f32, A/B f16, both K-major, M = 128, N = 64 / 128
+constexpr uint32_t kIdescN64 = (1u << 4) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescN128 = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void t5_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t acc,
+                                          uint32_t idesc = kIdescN64) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n}" ::"r"(d),
-      "l"(a), "l"(b), "r"(acc), "r"(kT5Idesc)
+      "l"(a), "l"(b), "r"(acc), "r"(idesc)
       : "memory");
+}
+
+// GEMM-completion wait: plain try_wait polling (no suspend hint: the GEMM takes
+// a few hundred cycles, a suspended warp may wake later than that), bounded
+// by %globaltimer like mbar_wait_bounded
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity, bool spin) {
+  if (!spin) {
+    mbar_wait_bounded(bar, parity);
+    return;
+  }
+  const uint32_t a = smem_addr(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const unsigned long long t0 = global_ns();
+  while (!mbar_try_wait(a, parity))
+    if (global_ns() - t0 > 4000000000ULL) __trap();
 }
 
 // fp16 hi/lo split of a (scaled) complex amplitude, stored as the f16x2 words
@@ -168,6 +188,22 @@ __device__ __forceinline__ void gemm_unpack(const uint32_t (&d)[32], float2 (&u)
   }
 }
 
+// One half when D is split over two accumulators (N128: columns 0..63 hold
+// Ah Bh + Al Bh, columns 64..127 hold Ah Bl): both loads in flight, summed.
+template <bool LD16>
+__device__ __forceinline__ void gemm_read_half_sum(uint32_t dcol, int half, float2 (&u)[16]) {
+  uint32_t d1[32], d2[32];
+  gemm_ld_issue<LD16>(dcol, half, d1);
+  gemm_ld_issue<LD16>(dcol + 64u, half, d2);
+  t5_wait_ld_tied(d1);
+  t5_wait_ld_tied(d2);
+  float2 v[16];
+  gemm_unpack<LD16>(d1, u);
+  gemm_unpack<LD16>(d2, v);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) u[q] = make_float2(u[q].x + v[q].x, u[q].y + v[q].y);
+}
+
 // Both halves of this thread's D row: two loads in flight, one wait.
 template <bool LD16>
 __device__ __forceinline__ void gemm_read_row(uint32_t dcol, float2 (&u0)[16], float2 (&u1)[16]) {
@@ -211,9 +247,12 @@ __device__ __forceinline__ void gemm_write_half(const float2 (&u)[16], uint32_t 
 // registers -> diagonal ops -> hi/lo A words of the next GEMM.
 // The halves a thread owns: both (4 warps per tile stream) or the one its
 // warp index selects (8 warps: register bit 4 becomes a warp bit).
-template <int NH, bool LD16>
+template <int NH, bool LD16, bool N128 = false>
 __device__ __forceinline__ void gemm_read_owned(uint32_t dcol, int h0, float2 (&u)[NH][16]) {
-  if constexpr (NH == 2) {
+  if constexpr (N128) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) gemm_read_half_sum<LD16>(dcol, h0 + k, u[k]);
+  } else if constexpr (NH == 2) {
     gemm_read_row<LD16>(dcol, u[0], u[1]);
   } else {
     uint32_t d[32];
@@ -223,13 +262,13 @@ __device__ __forceinline__ void gemm_read_owned(uint32_t dcol, int h0, float2 (&
   }
 }
 
-template <int NH, bool LD16>
+template <int NH, bool LD16, bool N128>
 __device__ __forceinline__ void gemm_phase_body(uint32_t dcol, const PassArgs<float2>& args,
                                                 const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
                                                 const int* dslot, int gt7, int h0, uint32_t wbase,
                                                 const uint32_t* wr) {
   float2 u[NH][16];
-  gemm_read_owned<NH, LD16>(dcol, h0, u);
+  gemm_read_owned<NH, LD16, N128>(dcol, h0, u);
 #pragma unroll
   for (int k = 0; k < NH; ++k) {
     const int half = h0 + k;
@@ -252,10 +291,10 @@ __device__ __forceinline__ float norm2_chains(const float2 (&u)[N]) {
   return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
-template <int NH, bool LD16>
+template <int NH, bool LD16, bool N128>
 __device__ __forceinline__ float gemm_norm_body(uint32_t dcol, int h0) {
   float2 u[NH][16];
-  gemm_read_owned<NH, LD16>(dcol, h0, u);
+  gemm_read_owned<NH, LD16, N128>(dcol, h0, u);
   float w = 0.f;
 #pragma unroll
   for (int k = 0; k < NH; ++k) w += norm2_chains(u[k]);
@@ -267,13 +306,14 @@ __device__ __forceinline__ float gemm_norm_body(uint32_t dcol, int h0) {
 // bit 0 (`pairs`), else 8-byte.
 // OFF: int when every offset of the tile fits 31 bits (n_local <= 31: one
 // IADD per store instead of a 64-bit add), else long long.
-template <int NH, bool LD16, class OFF>
-__device__ __forceinline__ void gemm_store_body(float2* __restrict__ dst, uint32_t dcol, const PassArgs<float2>& args,
+template <int NH, bool LD16, bool N128, class OFF>
+__device__ __forceinline__ float gemm_store_body(float2* __restrict__ dst, uint32_t dcol, const PassArgs<float2>& args,
                                                 const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
                                                 const int* dslot, int gt7, int h0, const long long* __restrict__ sr,
                                                 float f, bool pairs) {
   float2 uu[NH][16];
-  gemm_read_owned<NH, LD16>(dcol, h0, uu);
+  gemm_read_owned<NH, LD16, N128>(dcol, h0, uu);
+  float wsum = 0.f;
 #pragma unroll
   for (int k = 0; k < NH; ++k) {
     const int half = h0 + k;
@@ -306,7 +346,9 @@ __device__ __forceinline__ void gemm_store_body(float2* __restrict__ dst, uint32
         dst[o] = make_float2(u[r].x * f, u[r].y * f);
       }
     }
+    wsum += norm2_chains(u);
   }
+  return wsum * f * f;  // norm^2 of what was stored (diagonal ops included)
 }
 
 // Address tables of the pass (threads 0..127 compute them once per CTA).
@@ -338,13 +380,17 @@ __device__ __forceinline__ void gemm_tables(GemmTables& t, const PassArgs<float2
 // NG tile streams of WPG warps: WPG 4 -> a thread holds 32 amplitudes (both
 // register halves); WPG 8 -> 16 (register bit 4 is warp bit 2 of the stream),
 // twice the warps per scheduler to hide the GEMM / TMEM / barrier latency.
-template <int NG, int WPG = 4>
+// N128: the hi products run as one N = 128 GEMM, Ah [Bh | Bl], plus Al Bh
+// (8 instead of 12 MMAs, 56 instead of 72 KB of operand reads per tile and
+// GEMM); 128 TMEM columns per stream, summed at read-out.
+template <int NG, int WPG = 4, bool N128 = true>
 __global__ void __launch_bounds__(NG * WPG * 32, 1)
     k_gemm_pass(float2* __restrict__ amps, const __grid_constant__ PassArgs<float2> args) {
   constexpr int NTG = WPG * 32;
   constexpr int NH = WPG == 8 ? 1 : 2;  // register halves per thread
   constexpr int T = kGemmT;
-  constexpr uint32_t kTmemCols = NG > 2 ? 256 : 128;
+  constexpr uint32_t kColsPerGroup = N128 ? 128 : 64;
+  constexpr uint32_t kTmemCols = NG * kColsPerGroup > 256 ? 512 : NG * kColsPerGroup > 128 ? 256 : 128;
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const GemmSmem lay = gemm_smem_layout(h, NG, smem_addr(smem));
@@ -394,7 +440,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
   __syncthreads();
   t5_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t dcol = tbase + uint32_t(group) * 64u + (uint32_t((wig & 3) * 32) << 16);  // this warp's D lanes
+  const uint32_t dcol = tbase + uint32_t(group) * kColsPerGroup + (uint32_t((wig & 3) * 32) << 16);  // this warp's D lanes
 
   const int n_tiles = int(h.n_tiles);
   const int mine = int(blockIdx.x) < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
@@ -440,14 +486,38 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
     return s;
   };
 
+  // deferred renormalisation: the previous pass's norm drift (see PassHeader)
+  float corr = 1.f;
+  if (h.normacc && h.pass_index > 0) {
+    const double in = h.normacc[2 * h.pass_index - 2], out = h.normacc[2 * h.pass_index - 1];
+    if (in > 0.0 && out > 0.0) corr = float(sqrt(in / out));
+  }
+  double acc_in = 0.0, acc_out = 0.0;  // this thread's norm^2 contributions (true units)
+  // stage timestamps (SVB_GEMM_TRACE): CTA 0, stream 0, thread 0, first 8 tiles x 16 events
+  unsigned long long* tr = (h.trace && blockIdx.x == 0 && group == 0 && gt == 0) ? h.trace : nullptr;
+  int tev = 0;
+  auto mark = [&](int it_) {
+    if (tr && it_ < 8 * NG && tev < 16) tr[(it_ / NG) * 16 + tev++] = clock64();
+  };
   uint32_t fpar = 0, mpar = 0;
   int xs = 0;
+  if (h.debug & 48) {  // profiling: stagger the streams' start (debug 16: 300 ns, 32: 600 ns per stream)
+    const unsigned long long t0 = global_ns(), d = (h.debug & 16 ? 300ull : 600ull) * group;
+    while (global_ns() - t0 < d) {
+    }
+  }
   if (wig == 0 && group < mine) load(group, 0);
   for (int it = group; it < mine; it += NG, xs ^= 1) {
     const int* dslot = dout + (group * 2 + xs) * kMaxOps;
-    mbar_wait(&full[group], fpar);
+    tev = 0;
+    mark(it);
+    if (h.debug & 8)
+      mbar_wait_spin(&full[group], fpar, true);
+    else
+      mbar_wait(&full[group], fpar);
     fpar ^= 1;
     const long long origin = orig[group * 2 + xs];
+    mark(it);  // 1: tile landed
 
     // ---- phase 0: linear tile -> registers (load layout), tile norm, scale,
     // ops_0, A of GEMM 1 written in place
@@ -491,16 +561,19 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
         if (lane == 0) red[group * 16 + wig] = w;
       }
       group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
+      mark(it);  // 2: loaded + norm
       n2in = sum_red(0);
       // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
       const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
       const int se = min(max(268 - ebits, 1), 253);
       S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
+      if (gt == 0) acc_in += double(n2in) * double(corr) * double(corr);
+      const float Sc = S * corr;
       const uint32_t wb0 = tab.wb[0][gt7];
 #pragma unroll
       for (int k = 0; k < NH; ++k) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[k][q] = make_float2(v[k][q].x * S, v[k][q].y * S);
+        for (int q = 0; q < 16; ++q) v[k][q] = make_float2(v[k][q].x * Sc, v[k][q].y * Sc);
         for (int o = p0.op_begin; o < p0.op_end; ++o)
           gemm_diag_half(v[k], args.ops[o], pool + args.ops[o].coeff_off,
                          int(dthr[o * 128 + gt7]) | (h.has_outside ? dslot[o] : 0), h0 + k);
@@ -510,6 +583,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
     fence_proxy_async_smem();
     t5_fence_before();
     group_bar<NG, NTG>(group);
+    mark(it);  // 3: A of GEMM 1 written
 
     for (int p = 1; p <= P; ++p) {
       const PhaseDesc& ph = args.phases[p];
@@ -517,61 +591,83 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
       if (gt == 0) {
         t5_fence_after();
         const uint32_t b0 = mats + uint32_t(ph.tc) * kMmaMatBytes;
+        const uint32_t dacc = tbase + uint32_t(group) * kColsPerGroup;
+        if (!(h.debug & 1)) {
+          if constexpr (N128) {
+            // Ah [Bh | Bl] (N 128: the packed B is exactly the N = 128 K-major
+            // matrix [Bh | Bl]), then Al Bh into columns 0..63
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
+            for (int ks = 0; ks < 4; ++ks)
+              t5_mma_ss(dacc, sw128_desc(abase + 32u * ks), t5_desc(b0 + 256u * ks, 128, 1024), ks ? 1u : 0u,
+                        kIdescN128);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint64_t ad = sw128_desc(abase + (t == 1 ? uint32_t(kGemmAWords * 4) : 0u) + 32u * ks);
-            const uint64_t bd = t5_desc(b0 + (t == 2 ? 8192u : 0u) + 256u * ks, 128, 1024);
-            t5_mma_ss(tbase + uint32_t(group) * 64u, ad, bd, (t | ks) ? 1u : 0u);
+            for (int ks = 0; ks < 4; ++ks)
+              t5_mma_ss(dacc, sw128_desc(abase + uint32_t(kGemmAWords * 4) + 32u * ks),
+                        t5_desc(b0 + 256u * ks, 128, 1024), 1u, kIdescN64);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const uint64_t ad = sw128_desc(abase + (t == 1 ? uint32_t(kGemmAWords * 4) : 0u) + 32u * ks);
+                const uint64_t bd = t5_desc(b0 + (t == 2 ? 8192u : 0u) + 256u * ks, 128, 1024);
+                t5_mma_ss(dacc, ad, bd, (t | ks) ? 1u : 0u);
+              }
           }
+        }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_addr(&mbar[group]))
                      : "memory");
       }
-      mbar_wait_bounded(&mbar[group], mpar);
+      mbar_wait_spin(&mbar[group], mpar, h.debug & 4);
       mpar ^= 1;
       t5_fence_after();
+      mark(it);  // GEMM p done
       if (p < P) {
         const uint32_t wb = abase | tab.wb[p][gt7];
-        if (ld16)
-          gemm_phase_body<NH, true>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
+        if (h.debug & 2)
+          ;
+        else if (ld16)
+          gemm_phase_body<NH, true, N128>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         else
-          gemm_phase_body<NH, false>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
+          gemm_phase_body<NH, false, N128>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         fence_proxy_async_smem();
         t5_fence_before();
         group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
+        mark(it);  // A of GEMM p + 1 written
         continue;
       }
       // ---- last GEMM done: the buffer is free, so this stream's next tile
       // loads while this one is stored
       if (wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
-      // tile 2-norm of the result (diagonal ops are unimodular: applied after)
-      {
-        float w = ld16 ? gemm_norm_body<NH, true>(dcol, h0) : gemm_norm_body<NH, false>(dcol, h0);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        if (lane == 0) red[group * 16 + 8 + wig] = w;
-      }
-      group_bar<NG, NTG>(group);
-      const float n2out = sum_red(8);
-      // undo the scale, restore the tile 2-norm (all ops unitary)
-      const float f = n2out > 0.f ? sqrtf(n2in * S * S / n2out) / S : 1.f / S;
+      // undo the scale (the drift correction happens in the next pass)
+      const float f = 1.f / S;
       float2* __restrict__ dst = amps + origin + tab.st[gt7];
       const bool pairs = ph.map[0] == 0;  // register bit 0 = tile bit 0: 16-byte stores
+      float w;
       if (small) {
         if (ld16)
-          gemm_store_body<NH, true, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, true, N128, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
         else
-          gemm_store_body<NH, false, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, false, N128, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
       } else {
         if (ld16)
-          gemm_store_body<NH, true, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, true, N128, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
+                                                         pairs);
         else
-          gemm_store_body<NH, false, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, false, N128, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
+                                                          pairs);
       }
+      acc_out += double(w);
+      mark(it);  // stored
       t5_fence_before();
     }
+  }
+  if (h.normacc) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc_out += __shfl_xor_sync(0xffffffffu, acc_out, o);
+    if (lane == 0) atomicAdd(&h.normacc[2 * h.pass_index + 1], acc_out);
+    if (gt == 0) atomicAdd(&h.normacc[2 * h.pass_index], acc_in);
   }
   __syncthreads();
   if (tid < 32) {

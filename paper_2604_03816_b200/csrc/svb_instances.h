@@ -21,10 +21,10 @@ extern template __global__ void k_reg_pass<double2, 3>(double2*, const __grid_co
 extern template __global__ void k_reg_pass<double2, 4>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_reg_pass<double2, 4, 7>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_reg_pass<double2, 4, 7, 3>(double2*, const __grid_constant__ PassArgs<double2>);
-extern template __global__ void k_gemm_pass<2, 4>(float2*, const __grid_constant__ PassArgs<float2>);
-extern template __global__ void k_gemm_pass<2, 8>(float2*, const __grid_constant__ PassArgs<float2>);
-extern template __global__ void k_gemm_pass<3, 4>(float2*, const __grid_constant__ PassArgs<float2>);
-extern template __global__ void k_gemm_pass<3, 8>(float2*, const __grid_constant__ PassArgs<float2>);
-extern template __global__ void k_gemm_pass<4, 4>(float2*, const __grid_constant__ PassArgs<float2>);
-extern template __global__ void k_gemm_pass<4, 8>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_reg_pass<double2, 4, 7, 4>(double2*, const __grid_constant__ PassArgs<double2>);
+extern template __global__ void k_gemm_pass<4, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_gemm_pass<4, 4, false>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_gemm_pass<3, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_gemm_pass<2, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_gemm_pass<4, 8, true>(float2*, const __grid_constant__ PassArgs<float2>);
 }  // namespace svb

@@ -41,15 +41,16 @@ __host__ __device__ constexpr int deposit_mask(int x, int mask) {
 __host__ __device__ constexpr int popc_c(int m) { return m ? (m & 1) + popc_c(m >> 1) : 0; }
 
 // Dense op on register bits MASK (matrix-local bit j <-> j-th lowest set bit).
-template <class C, int RB, int MASK>
+template <class C, int RB, int MASK, bool HOIST = true>
 __device__ __forceinline__ void reg_dense(C (&v)[1 << RB], const C* __restrict__ Ms) {
   constexpr int K = popc_c(MASK);
   constexpr int D = 1 << K;
   constexpr int REST = ((1 << RB) - 1) & ~MASK;
   // matrices up to 2q (c64 and c128) are hoisted into registers (measured:
-  // per-use shared-memory broadcasts cost 12% on layered c128); wider ones
-  // are read per use
-  constexpr bool kHoist = D <= 4;
+  // per-use shared-memory broadcasts cost 12% on layered c128 at 3 streams);
+  // wider ones, and every one in the 4-stream c128 kernel (128 registers),
+  // are read per use (shared-memory broadcasts)
+  constexpr bool kHoist = HOIST && D <= 4;
   C M[kHoist ? D * D : 1];
   if constexpr (kHoist) {
 #pragma unroll
@@ -137,13 +138,13 @@ __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, cons
   }
 }
 
-template <class C, int RB>
+template <class C, int RB, bool HOIST = true>
 __device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool) {
   const C* co = pool + op.coeff_off;
   switch (op.pad) {  // register-bit mask of the dense op
 #define SVB_CASE(m) \
   case m:           \
-    if constexpr ((m) < (1 << RB) && popc_c(m) <= 3) reg_dense<C, RB, (m)>(v, co); \
+    if constexpr ((m) < (1 << RB) && popc_c(m) <= 3) reg_dense<C, RB, (m), HOIST>(v, co); \
     break;
     SVB_CASE(1) SVB_CASE(2) SVB_CASE(3) SVB_CASE(4) SVB_CASE(5) SVB_CASE(6) SVB_CASE(7)
     SVB_CASE(8) SVB_CASE(9) SVB_CASE(10) SVB_CASE(11) SVB_CASE(12) SVB_CASE(13) SVB_CASE(14)
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
           reg_diag<C, RB>(v, op, pool + op.coeff_off,
                           int(dthr[o * NTG + gt]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
         else
-          reg_dense_op<C, RB>(v, op, pool);
+          reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4)>(v, op, pool);
       }
       if constexpr (sizeof(C) == 8 && RB == 5) {
         if (last && h.renorm) {

@@ -98,6 +98,16 @@ struct PassHeader {
   int thread_bits;              // k_reg_pass: 8 (one tile stream) or 7 (warp groups of 128)
   int streams;                  // k_reg_pass with 7 thread bits: 2 or 3 tile streams
   int gemm;                     // k_gemm_pass (PhaseDesc::R holds the A word table)
+  int debug;                    // k_gemm_pass profiling switches (SVB_GEMM_DEBUG): 1 no MMAs,
+                                // 2 no intermediate D -> A conversions (wrong results)
+  unsigned long long* trace;    // k_gemm_pass stage timestamps of CTA 0 / stream 0 (or null)
+  // k_gemm_pass norm bookkeeping (deferred renormalisation): pass k adds its
+  // input norm^2 (after its own correction) to normacc[2k] and its output
+  // norm^2 to normacc[2k + 1]; pass k + 1 multiplies its input by
+  // sqrt(normacc[2k] / normacc[2k + 1]) -- the tensor cores' fp32 truncation
+  // loss of pass k (~1e-6 per GEMM) -- folded into its scale factor
+  double* normacc;
+  int pass_index;
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)
