@@ -89,6 +89,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_reg_pass<float2, 3>,   (const void*)k_reg_pass<float2, 4>,
                          (const void*)k_reg_pass<float2, 5>,   (const void*)k_gemm_pass<4, 4, true>,
                          (const void*)k_gemm_pass<4, 4, false>, (const void*)k_gemm_pass<3, 4, true>,
+                         (const void*)k_gemm_pass<5, 4, false>,
                          (const void*)k_gemm_pass<2, 4, true>, (const void*)k_gemm_pass<4, 8, true>,
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
@@ -314,14 +315,31 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
       a.h.trace = trace;
       g_trace = trace;
       const int wpg = a.h.gemm == 8 ? 8 : 4;  // warps per tile stream
-      const int ng = wpg == 8 ? 4 : a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
+      int ng = wpg == 8 ? 4 : a.h.streams == 2 ? 2 : a.h.streams == 3 ? 3 : 4;
+      // five tile streams (passes with <= 3 GEMMs fit shared memory) only on
+      // request, SVB_GEMM_DEBUG bit 2048: measured 16.9 vs 16.4 ms -- the
+      // 96-register budget of 640 threads (spills, one TMEM half in flight)
+      // costs more than the fifth tile in flight gains
+      if (ng == 4 && wpg == 4 && (dbg & 2048)) {
+        a.h.gemm_bufs = 5;
+        if (gemm_smem_layout(a.h, 5, f->dyn_smem_base).total <= size_t(f->max_smem)) ng = 5;
+      }
       // SVB_GEMM_DEBUG bit 256: the 8-MMA (N = 128 hi product) variant, for comparison
       // (measured slower: 17.1 vs 16.2 ms, the doubled TMEM read-out costs more)
       void (*gfn)(float2*, PassArgs<float2>) =
           wpg == 8 ? k_gemm_pass<4, 8, true>
+          : ng == 5 ? k_gemm_pass<5, 4, false>
           : ng == 2 ? k_gemm_pass<2, 4, true>
           : ng == 3 ? k_gemm_pass<3, 4, true>
           : (dbg & 256) ? k_gemm_pass<4, 4, true> : k_gemm_pass<4, 4, false>;
+      // a spare tile buffer when shared memory allows (loads issued one tile
+      // slot ahead; measured neutral at four streams) -- only on request,
+      // SVB_GEMM_DEBUG bit 4096
+      a.h.gemm_bufs = ng;
+      if ((dbg & 4096) && gemm_smem_layout(a.h, ng, f->dyn_smem_base).total <= size_t(f->max_smem)) {
+        a.h.gemm_bufs = ng + 1;
+        if (gemm_smem_layout(a.h, ng, f->dyn_smem_base).total > size_t(f->max_smem)) a.h.gemm_bufs = ng;
+      }
       const size_t smem_g = gemm_smem_layout(a.h, ng, f->dyn_smem_base).total;
       if (smem_g > size_t(f->max_smem)) return fail(SVB_EUNSUPPORTED, "gemm pass exceeds shared memory");
       long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count);

@@ -64,7 +64,7 @@ struct GemmTables {
 };
 
 struct GemmSmem {
-  size_t pool, dthr, dout, red, orig, tabs, mats, tiles, total;
+  size_t pool, dthr, dout, red, orig, iss, tabs, mats, tiles, total;
 };
 // `base` = shared-window address of the dynamic shared memory (the tile
 // buffers are placed 16 KB-aligned in that window so that an A word's byte
@@ -73,13 +73,15 @@ __host__ __device__ inline GemmSmem gemm_smem_layout(const PassHeader& h, int ng
   GemmSmem l;
   l.pool = 128;  // barriers + TMEM slot
   l.dthr = l.pool + align_up(size_t(h.coeff_count) * sizeof(float2), 128);
+  const int nb = h.gemm_bufs > ng ? h.gemm_bufs : ng;  // tile buffers (ring)
   l.dout = l.dthr + align_up(size_t(h.n_ops) * 128, 128);
-  l.red = l.dout + align_up(size_t(ng) * 2 * kMaxOps * sizeof(int), 128);
+  l.red = l.dout + align_up(size_t(nb) * 2 * kMaxOps * sizeof(int), 128);
   l.orig = align_up(l.red + size_t(ng) * 16 * sizeof(float), 128);
-  l.tabs = align_up(l.orig + size_t(ng) * 2 * sizeof(long long), 128);
+  l.iss = align_up(l.orig + size_t(nb) * 2 * sizeof(long long), 128);
+  l.tabs = align_up(l.iss + size_t(nb) * sizeof(int), 128);
   l.mats = align_up(l.tabs + sizeof(GemmTables), 1024);
   l.tiles = align_up(base + l.mats + size_t(h.tc_count) * kMmaMatBytes, 16384) - base;
-  l.total = l.tiles + size_t(ng) * kGemmTileBytes;
+  l.total = l.tiles + size_t(nb) * kGemmTileBytes;
   return l;
 }
 
@@ -247,9 +249,17 @@ __device__ __forceinline__ void gemm_write_half(const float2 (&u)[16], uint32_t 
 // registers -> diagonal ops -> hi/lo A words of the next GEMM.
 // The halves a thread owns: both (4 warps per tile stream) or the one its
 // warp index selects (8 warps: register bit 4 becomes a warp bit).
-template <int NH, bool LD16, bool N128 = false>
+template <int NH, bool LD16, bool N128 = false, bool SEQ = false>
 __device__ __forceinline__ void gemm_read_owned(uint32_t dcol, int h0, float2 (&u)[NH][16]) {
-  if constexpr (N128) {
+  if constexpr (SEQ && !N128) {
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      uint32_t d[32];
+      gemm_ld_issue<LD16>(dcol, h0 + k, d);
+      t5_wait_ld_tied(d);
+      gemm_unpack<LD16>(d, u[k]);
+    }
+  } else if constexpr (N128) {
 #pragma unroll
     for (int k = 0; k < NH; ++k) gemm_read_half_sum<LD16>(dcol, h0 + k, u[k]);
   } else if constexpr (NH == 2) {
@@ -262,20 +272,34 @@ __device__ __forceinline__ void gemm_read_owned(uint32_t dcol, int h0, float2 (&
   }
 }
 
-template <int NH, bool LD16, bool N128>
+template <int NH, bool LD16, bool N128, bool SEQ = false>
 __device__ __forceinline__ void gemm_phase_body(uint32_t dcol, const PassArgs<float2>& args,
                                                 const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
                                                 const int* dslot, int gt7, int h0, uint32_t wbase,
                                                 const uint32_t* wr) {
-  float2 u[NH][16];
-  gemm_read_owned<NH, LD16, N128>(dcol, h0, u);
+  if constexpr (SEQ) {
+    // one half in registers at a time (the 5-stream kernel's register budget)
 #pragma unroll
-  for (int k = 0; k < NH; ++k) {
-    const int half = h0 + k;
-    for (int o = ph.op_begin; o < ph.op_end; ++o)
-      gemm_diag_half(u[k], args.ops[o], pool + args.ops[o].coeff_off,
-                     int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
-    gemm_write_half(u[k], wbase, wr, half);
+    for (int k = 0; k < NH; ++k) {
+      const int half = h0 + k;
+      float2 u[1][16];
+      gemm_read_owned<1, LD16, N128, true>(dcol, half, u);
+      for (int o = ph.op_begin; o < ph.op_end; ++o)
+        gemm_diag_half(u[0], args.ops[o], pool + args.ops[o].coeff_off,
+                       int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
+      gemm_write_half(u[0], wbase, wr, half);
+    }
+  } else {
+    float2 u[NH][16];
+    gemm_read_owned<NH, LD16, N128>(dcol, h0, u);
+#pragma unroll
+    for (int k = 0; k < NH; ++k) {
+      const int half = h0 + k;
+      for (int o = ph.op_begin; o < ph.op_end; ++o)
+        gemm_diag_half(u[k], args.ops[o], pool + args.ops[o].coeff_off,
+                       int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
+      gemm_write_half(u[k], wbase, wr, half);
+    }
   }
 }
 
@@ -306,18 +330,19 @@ __device__ __forceinline__ float gemm_norm_body(uint32_t dcol, int h0) {
 // bit 0 (`pairs`), else 8-byte.
 // OFF: int when every offset of the tile fits 31 bits (n_local <= 31: one
 // IADD per store instead of a 64-bit add), else long long.
-template <int NH, bool LD16, bool N128, class OFF>
+template <int NH, bool LD16, bool N128, class OFF, bool SEQ = false>
 __device__ __forceinline__ float gemm_store_body(float2* __restrict__ dst, uint32_t dcol, const PassArgs<float2>& args,
                                                 const PhaseDesc& ph, const float2* pool, const unsigned char* dthr,
                                                 const int* dslot, int gt7, int h0, const long long* __restrict__ sr,
                                                 float f, bool pairs) {
-  float2 uu[NH][16];
-  gemm_read_owned<NH, LD16, N128>(dcol, h0, uu);
+  float2 uu[SEQ ? 1 : NH][16];
+  if constexpr (!SEQ) gemm_read_owned<NH, LD16, N128>(dcol, h0, uu);
   float wsum = 0.f;
 #pragma unroll
   for (int k = 0; k < NH; ++k) {
     const int half = h0 + k;
-    float2 (&u)[16] = uu[k];
+    if constexpr (SEQ) gemm_read_owned<1, LD16, N128, true>(dcol, half, uu);
+    float2 (&u)[16] = uu[SEQ ? 0 : k];
     for (int o = ph.op_begin; o < ph.op_end; ++o)
       gemm_diag_half(u, args.ops[o], pool + args.ops[o].coeff_off,
                      int(dthr[o * 128 + gt7]) | (args.h.has_outside ? dslot[o] : 0), half);
@@ -388,20 +413,27 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
     k_gemm_pass(float2* __restrict__ amps, const __grid_constant__ PassArgs<float2> args) {
   constexpr int NTG = WPG * 32;
   constexpr int NH = WPG == 8 ? 1 : 2;  // register halves per thread
+  constexpr bool SEQ = NG >= 5;         // 640 threads: one register half in flight
   constexpr int T = kGemmT;
   constexpr uint32_t kColsPerGroup = N128 ? 128 : 64;
   constexpr uint32_t kTmemCols = NG * kColsPerGroup > 256 ? 512 : NG * kColsPerGroup > 128 ? 256 : 128;
+  static_assert(NG * kColsPerGroup <= 512, "TMEM columns");
   extern __shared__ __align__(1024) unsigned char smem[];
   const PassHeader& h = args.h;
   const GemmSmem lay = gemm_smem_layout(h, NG, smem_addr(smem));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [group] tile landed
-  uint64_t* mbar = full + NG;                           // [group] GEMM committed
+  const int NB = h.gemm_bufs > NG ? h.gemm_bufs : NG;  // tile buffers: tile t -> buffer t % NB
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [buffer] tile landed
+  uint64_t* mbar = full + 8;                            // [group] GEMM committed (<= 6)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + NG);
   float2* pool = reinterpret_cast<float2*>(smem + lay.pool);
   unsigned char* dthr = smem + lay.dthr;                 // [op][thread] diagonal index, thread part
-  int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [group][2][op] outside-tile part
+  int* dout = reinterpret_cast<int*>(smem + lay.dout);  // [buffer][2][op] outside-tile part
   float* red = reinterpret_cast<float*>(smem + lay.red);  // [group][in 8 | out 8] norm partials
-  long long* orig = reinterpret_cast<long long*>(smem + lay.orig);  // [group][2] tile origins
+  long long* orig = reinterpret_cast<long long*>(smem + lay.orig);  // [buffer][2] tile origins
+  // [buffer] the tile whose load was last issued into it: a stream waits for
+  // its tile's load to be issued before it waits on the buffer's mbarrier
+  // parity (with a spare buffer a stream can run one use ahead of a buffer)
+  volatile int* iss = reinterpret_cast<volatile int*>(smem + lay.iss);
   const uint32_t mats = smem_addr(smem + lay.mats);
   unsigned char* tiles = smem + lay.tiles;
   const int tid = threadIdx.x;
@@ -411,10 +443,11 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
   const int P = h.n_phases - 1;  // GEMM phases
 
   if (tid == 0) {
-    for (int g = 0; g < NG; ++g) {
-      mbar_init(&full[g], 1);
-      mbar_init(&mbar[g], 1);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      iss[b] = -1;
     }
+    for (int g = 0; g < NG; ++g) mbar_init(&mbar[g], 1);
     fence_mbar_init();
   }
   if (tid < 32) {
@@ -444,26 +477,31 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
 
   const int n_tiles = int(h.n_tiles);
   const int mine = int(blockIdx.x) < n_tiles ? (n_tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1 : 0;
-  float2* buf = reinterpret_cast<float2*>(tiles + size_t(group) * kGemmTileBytes);
-  const uint32_t abase = smem_addr(buf);  // 16 KB aligned (gemm_smem_layout)
-  if (abase & 16383u) __trap();          // host and device disagree on the shared window
+  if (smem_addr(tiles) & 16383u) __trap();  // host and device disagree on the shared window
   // every shard offset of a tile fits 31 bits (int store offsets)
   const bool small = (h.m == 0 ? h.L : h.high_sorted[h.m - 1] + 1) <= 31;
 
-  // the stream's tile load (warp 0 of the group: lane 0 issues the TMA, all
-  // lanes publish the tile origin and the outside-tile diagonal index parts)
-  auto load = [&](int it, int xs) {
-    const int tile = int(blockIdx.x) + it * int(gridDim.x);
+  // Tile t (this CTA's t-th tile, processed by stream t % NG) lands in buffer
+  // t % NB.  With a spare buffer (NB = NG + 1) the load of tile t is issued
+  // when tile t - NB leaves its buffer (after its last GEMM), one tile slot
+  // ahead of the stream that needs it: the HBM latency hides behind other
+  // work.  Issued by warp 0 of the freeing stream (lane 0 issues the TMA, all
+  // lanes publish the tile origin and the outside-tile diagonal index parts).
+  auto load = [&](int t) {
+    const int tile = int(blockIdx.x) + t * int(gridDim.x);
+    const int b = t % NB, xs = (t / NB) & 1;
+    float2* lbuf = reinterpret_cast<float2*>(tiles + size_t(b) * kGemmTileBytes);
     const long long tb = tile_base(tile, h);
-    if (lane == 0) orig[group * 2 + xs] = tb;  // published with the tile (mbarrier release)
+    if (lane == 0) orig[b * 2 + xs] = tb;  // published with the tile (mbarrier release)
     if (h.has_outside) {
-      int* slot = dout + (group * 2 + xs) * kMaxOps;
+      int* slot = dout + (b * 2 + xs) * kMaxOps;
       for (int i = lane; i < h.n_ops; i += 32)
         slot[i] = args.ops[i].kind == OP_DIAG ? diag_outside_part(args.ops[i], tb) : 0;
     }
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive_expect_tx(&full[group], uint32_t(kGemmTileBytes));
+      mbar_arrive_expect_tx(&full[b], uint32_t(kGemmTileBytes));
+      iss[b] = t;
       const int ne = h.n_enum;
       const int sub = T - ne;
       for (int e = 0; e < (1 << ne); ++e) {
@@ -474,7 +512,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
 #pragma unroll
         for (int d = 0; d < 5; ++d)
           c[d] = (d < h.tma_rank && h.tma_box[d] == 0) ? int((origin >> h.tma_start[d]) & ((1LL << h.tma_bits[d]) - 1)) : 0;
-        tma_load(buf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[group]);
+        tma_load(lbuf + (size_t(e) << sub), &args.tmap, c, h.tma_rank, &full[b]);
       }
     }
     __syncwarp();
@@ -499,24 +537,29 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
   auto mark = [&](int it_) {
     if (tr && it_ < 8 * NG && tev < 16) tr[(it_ / NG) * 16 + tev++] = clock64();
   };
-  uint32_t fpar = 0, mpar = 0;
-  int xs = 0;
+  uint32_t mpar = 0;
   if (h.debug & 48) {  // profiling: stagger the streams' start (debug 16: 300 ns, 32: 600 ns per stream)
     const unsigned long long t0 = global_ns(), d = (h.debug & 16 ? 300ull : 600ull) * group;
     while (global_ns() - t0 < d) {
     }
   }
-  if (wig == 0 && group < mine) load(group, 0);
-  for (int it = group; it < mine; it += NG, xs ^= 1) {
-    const int* dslot = dout + (group * 2 + xs) * kMaxOps;
+  if (group == 0 && wig == 0)
+    for (int t = 0; t < NB && t < mine; ++t) load(t);
+  for (int it = group; it < mine; it += NG) {
+    const int bi = it % NB, xs = (it / NB) & 1;
+    const uint32_t fpar = uint32_t(xs);
+    float2* buf = reinterpret_cast<float2*>(tiles + size_t(bi) * kGemmTileBytes);
+    const uint32_t abase = smem_addr(buf);  // 16 KB aligned (gemm_smem_layout)
+    const int* dslot = dout + (bi * 2 + xs) * kMaxOps;
+    if (NB != NG)
+      while (iss[bi] != it) __nanosleep(20);
     tev = 0;
     mark(it);
     if (h.debug & 8)
-      mbar_wait_spin(&full[group], fpar, true);
+      mbar_wait_spin(&full[bi], fpar, true);
     else
-      mbar_wait(&full[group], fpar);
-    fpar ^= 1;
-    const long long origin = orig[group * 2 + xs];
+      mbar_wait(&full[bi], fpar);
+    const long long origin = orig[bi * 2 + xs];
     mark(it);  // 1: tile landed
 
     // ---- phase 0: linear tile -> registers (load layout), tile norm, scale,
@@ -628,9 +671,9 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
         if (h.debug & 2)
           ;
         else if (ld16)
-          gemm_phase_body<NH, true, N128>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
+          gemm_phase_body<NH, true, N128, SEQ>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         else
-          gemm_phase_body<NH, false, N128>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
+          gemm_phase_body<NH, false, N128, SEQ>(dcol, args, ph, pool, dthr, dslot, gt7, h0, wb, tab.wr[p]);
         fence_proxy_async_smem();
         t5_fence_before();
         group_bar<NG, NTG>(group);  // A complete; every D read done before the next GEMM
@@ -639,7 +682,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
       }
       // ---- last GEMM done: the buffer is free, so this stream's next tile
       // loads while this one is stored
-      if (wig == 0 && it + NG < mine) load(it + NG, xs ^ 1);
+      if (wig == 0 && it + NB < mine) load(it + NB);
       // undo the scale (the drift correction happens in the next pass)
       const float f = 1.f / S;
       float2* __restrict__ dst = amps + origin + tab.st[gt7];
@@ -647,15 +690,15 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
       float w;
       if (small) {
         if (ld16)
-          w = gemm_store_body<NH, true, N128, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, true, N128, int, SEQ>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
         else
-          w = gemm_store_body<NH, false, N128, int>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
+          w = gemm_store_body<NH, false, N128, int, SEQ>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f, pairs);
       } else {
         if (ld16)
-          w = gemm_store_body<NH, true, N128, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
+          w = gemm_store_body<NH, true, N128, long long, SEQ>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
                                                          pairs);
         else
-          w = gemm_store_body<NH, false, N128, long long>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
+          w = gemm_store_body<NH, false, N128, long long, SEQ>(dst, dcol, args, ph, pool, dthr, dslot, gt7, h0, tab.str, f,
                                                           pairs);
       }
       acc_out += double(w);

@@ -24,6 +24,7 @@ extern template __global__ void k_reg_pass<double2, 4, 7, 3>(double2*, const __g
 extern template __global__ void k_reg_pass<double2, 4, 7, 4>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_gemm_pass<4, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
 extern template __global__ void k_gemm_pass<4, 4, false>(float2*, const __grid_constant__ PassArgs<float2>);
+extern template __global__ void k_gemm_pass<5, 4, false>(float2*, const __grid_constant__ PassArgs<float2>);
 extern template __global__ void k_gemm_pass<3, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
 extern template __global__ void k_gemm_pass<2, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
 extern template __global__ void k_gemm_pass<4, 8, true>(float2*, const __grid_constant__ PassArgs<float2>);

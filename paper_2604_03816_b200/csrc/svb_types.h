@@ -108,6 +108,7 @@ struct PassHeader {
   // loss of pass k (~1e-6 per GEMM) -- folded into its scale factor
   double* normacc;
   int pass_index;
+  int gemm_bufs;                // k_gemm_pass tile buffers (ring; >= streams)
 };
 
 // opaque 128-byte CUtensorMap (filled at launch time by the host)
