@@ -71,6 +71,8 @@ typedef struct svb_plan_options {
                            producer warp), 1 = one stream of 256; 0 = default
                            (4 for c64 tensor-core phases, 3 for c128)           */
   int gemm_warps;       /* k_gemm_pass warps per tile stream: 4 or 8 (0: default 4) */
+  int no_factor;        /* c128: -1 = factor fused 2q gates as D P (A x B) where cheaper
+                           (structured 1q ops + CNOT permutation); 0/1 = keep them dense */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */

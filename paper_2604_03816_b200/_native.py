@@ -35,7 +35,8 @@ class PlanOptions(C.Structure):
                 ("max_ops_per_pass", C.c_int), ("cost_budget", C.c_double),
                 ("no_diag_merge", C.c_int), ("stages", C.c_int), ("reg_bits", C.c_int),
                 ("no_reg_phases", C.c_int), ("tensor_cores", C.c_int), ("tc_min_dense", C.c_int),
-                ("no_window_search", C.c_int), ("streams", C.c_int), ("gemm_warps", C.c_int)]
+                ("no_window_search", C.c_int), ("streams", C.c_int), ("gemm_warps", C.c_int),
+                ("no_factor", C.c_int)]
 
 
 class PassInfo(C.Structure):
@@ -47,6 +48,7 @@ class PassInfo(C.Structure):
 
 
 KERNELS = ("tile", "reg", "reg_tc", "gemm")
+KINDS = ("dense", "diag", "perm")  # OpKind; "perm" = CNOT, targets (control, target)
 
 
 class NativeError(RuntimeError):
@@ -184,8 +186,10 @@ class NativePlan:
         co = np.zeros(2 * 4096, dtype=np.float64)
         n = check(lib().svb_plan_phase_op(self._h, p, i, C.byref(kind), C.byref(k), C.byref(mask),
                                           _iptr(src), _dptr(co), 4096))
-        out = {"kind": "diag" if kind.value == 1 else "dense", "k": k.value, "mask": mask.value,
+        out = {"kind": KINDS[kind.value], "k": k.value, "mask": mask.value,
                "coeffs": co[:2 * n].view(np.complex128).copy()}
+        if kind.value == 2:  # CNOT: control / target register bits
+            out["ctrl"], out["tgt"] = int(src[0]), int(src[1])
         if kind.value == 1:
             out["thread_bits"] = [int(x) for x in src[:mask.value]]
             out["rmap"] = src[8:16].view(np.uint8).copy()
@@ -207,7 +211,7 @@ class NativePlan:
         n = check(lib().svb_plan_kernel_op(self._h, p, i, C.byref(kind), C.byref(k), _iptr(tg),
                                            _dptr(co), 4096))
         coeffs = co[:2 * n].view(np.complex128).copy()
-        return {"kind": "diag" if kind.value == 1 else "dense", "k": k.value,
+        return {"kind": KINDS[kind.value], "k": k.value,
                 "targets": [int(t) for t in tg[:k.value]], "coeffs": coeffs}
 
     def execute(self, amps_ptr: int, stream: int, first: int = 0, count: int | None = None):

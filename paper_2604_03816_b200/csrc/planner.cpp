@@ -120,6 +120,132 @@ struct DiagAcc {
 
 size_t coeff_elems(const KernelOp& op) { return op.coeff.size(); }
 
+// ------------------------------------------------- 2q gate factorisation (c128)
+// A fused 2-qubit gate from dag.fuse is stored as a dense 4x4 matrix (16 FP64
+// FMAs per amplitude in the register kernel, which is FP64-bound for c128).
+// Layered circuits fuse (RZ x RZ) CNOT (G x G'), G in {H, RX, RZ}: factor
+//   U = D P (A x B),  D diagonal, P in {I, CNOT 0->1, CNOT 1->0},
+// normalise the rows of A and B (first non-zero entry real positive; the row
+// phases move into D), and apply A, B as 1-qubit ops whose columns are purely
+// real or imaginary where possible (4 instead of 8 FMAs per amplitude), P as
+// a register permutation and D through the diagonal-run merge.
+struct Factor2q {
+  int perm = 0;                 // 0: none, 1: CNOT control bit 0 -> target 1, 2: control 1 -> target 0
+  std::vector<cd> A, B;         // 2x2 row-major (local bit 0: A, local bit 1: B)
+  bool a_id = false, b_id = false;
+  int a_st = ST_GENERAL, b_st = ST_GENERAL;
+  std::vector<cd> d;            // 4 diagonal entries (local bits 0, 1)
+};
+
+int col_structure(const std::vector<cd>& m) {
+  auto kind = [&](int c) {  // 1 real, 2 imag, 0 complex (column c of a 2x2)
+    bool re = true, im = true;
+    for (int r = 0; r < 2; ++r) {
+      re = re && std::abs(m[size_t(r) * 2 + c].imag()) <= 1e-15;
+      im = im && std::abs(m[size_t(r) * 2 + c].real()) <= 1e-15;
+    }
+    return re ? 1 : im ? 2 : 0;
+  };
+  const int c0 = kind(0), c1 = kind(1);
+  if (!c0 || !c1) return ST_GENERAL;
+  return c0 == 1 ? (c1 == 1 ? ST_RR : ST_RI) : (c1 == 1 ? ST_IR : ST_II);
+}
+
+bool factor_2q(const std::vector<cd>& U, Factor2q& f) {
+  auto permute = [](int x, int pm) {
+    if (pm == 1) return x ^ ((x & 1) << 1);
+    if (pm == 2) return x ^ ((x >> 1) & 1);
+    return x;
+  };
+  for (int pm = 0; pm < 3; ++pm) {
+    cd W[4][4];
+    for (int x = 0; x < 4; ++x)
+      for (int y = 0; y < 4; ++y) W[x][y] = U[size_t(permute(x, pm)) * 4 + y];
+    // row x = (xa | xb << 1) ~ d'_x (A[xa, :] x B[xb, :]), column y = ya | yb << 1
+    cd A[2][2], B[2][2];
+    bool ok = true;
+    for (int xa = 0; xa < 2 && ok; ++xa) {  // A rows from rows xb = 0, B rows from rows xa = 0
+      int ya = 0, yb = 0;
+      double best = -1;
+      for (int y = 0; y < 4; ++y)
+        if (std::abs(W[xa][y]) > best) {
+          best = std::abs(W[xa][y]);
+          ya = y & 1;
+          yb = y >> 1;
+        }
+      if (best < 1e-12) ok = false;
+      for (int j = 0; j < 2; ++j) A[xa][j] = W[xa][j | yb << 1];
+      (void)ya;
+    }
+    for (int xb = 0; xb < 2 && ok; ++xb) {
+      int ya = 0;
+      double best = -1;
+      for (int y = 0; y < 4; ++y)
+        if (std::abs(W[xb << 1][y]) > best) {
+          best = std::abs(W[xb << 1][y]);
+          ya = y & 1;
+        }
+      if (best < 1e-12) ok = false;
+      for (int j = 0; j < 2; ++j) B[xb][j] = W[xb << 1][ya | j << 1];
+    }
+    if (!ok) continue;
+    auto normalise = [](cd (&m)[2][2]) {
+      for (int r = 0; r < 2; ++r) {
+        int j0 = std::abs(m[r][0]) > 1e-12 ? 0 : 1;
+        const cd ph = m[r][j0] / std::abs(m[r][j0]);
+        const double nrm = std::sqrt(std::norm(m[r][0]) + std::norm(m[r][1]));
+        for (int j = 0; j < 2; ++j) m[r][j] /= ph * nrm;
+      }
+    };
+    normalise(A);
+    normalise(B);
+    // D' per row from the largest entry, then verify the whole matrix
+    cd dp[4];
+    double err = 0.0;
+    for (int x = 0; x < 4; ++x) {
+      const int xa = x & 1, xb = x >> 1;
+      int yb_ = 0;
+      double best = -1;
+      for (int y = 0; y < 4; ++y)
+        if (std::abs(W[x][y]) > best) {
+          best = std::abs(W[x][y]);
+          yb_ = y;
+        }
+      const cd den = A[xa][yb_ & 1] * B[xb][yb_ >> 1];
+      if (std::abs(den) < 1e-12) {
+        err = 1.0;
+        break;
+      }
+      dp[x] = W[x][yb_] / den;
+      for (int y = 0; y < 4; ++y) err = std::max(err, std::abs(W[x][y] - dp[x] * A[xa][y & 1] * B[xb][y >> 1]));
+    }
+    if (err > 1e-13) continue;
+    f.perm = pm;
+    f.A.assign({A[0][0], A[0][1], A[1][0], A[1][1]});
+    f.B.assign({B[0][0], B[0][1], B[1][0], B[1][1]});
+    auto is_id = [](const std::vector<cd>& m) {
+      return std::abs(m[0] - 1.0) <= 1e-15 && std::abs(m[3] - 1.0) <= 1e-15 && std::abs(m[1]) <= 1e-15 &&
+             std::abs(m[2]) <= 1e-15;
+    };
+    f.a_id = is_id(f.A);
+    f.b_id = is_id(f.B);
+    f.a_st = col_structure(f.A);
+    f.b_st = col_structure(f.B);
+    // U = D P (A x B): d[perm(x)] = d'_x
+    f.d.assign(4, cd());
+    for (int x = 0; x < 4; ++x) f.d[permute(x, pm)] = dp[x];
+    return true;
+  }
+  return false;
+}
+
+// FP64 FMAs per amplitude of the factored form (diagonal counted as a
+// complex multiply; it usually merges with neighbouring diagonal runs)
+double factored_cost(const Factor2q& f) {
+  auto one = [](bool id, int st) { return id ? 0.0 : st == ST_GENERAL ? 8.0 : 4.0; };
+  return one(f.a_id, f.a_st) + one(f.b_id, f.b_st) + 4.0;
+}
+
 // Transposes around the first / last phase: the TMA buffer (linear tile
 // layout) is read, and the last phase stores to HBM, directly in the phase's
 // layout only when the lane bits cover the bank-row index bits (conflict-free
@@ -168,10 +294,10 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       int bits = 0;
       for (int j = 0; j < op.k; ++j)
         if (op.tgt[j] < p.T) bits |= 1 << op.tgt[j];
-      const bool blocked = (bits & all_block) || (op.kind == OP_DENSE && (bits & dense_block));
+      const bool blocked = (bits & all_block) || (op.kind != OP_DIAG && (bits & dense_block));
       const bool take = !blocked && (op.kind == OP_DIAG || (bits & ~mask) == 0);
       if (take) {
-        dense += op.kind == OP_DENSE;
+        dense += op.kind != OP_DIAG;
       } else {
         (op.kind == OP_DIAG ? dense_block : all_block) |= bits;
       }
@@ -187,7 +313,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
     // First-fit order decides only when fewer than RB bits are in play.
     int cand = 0;
     for (int i : pending)
-      if (p.ops[i].kind == OP_DENSE)
+      if (p.ops[i].kind != OP_DIAG)
         for (int j = 0; j < p.ops[i].k; ++j) cand |= 1 << p.ops[i].tgt[j];
     int fixed = -1;
     if (__builtin_popcount(cand) > RB && __builtin_popcount(cand) <= 16) {
@@ -220,7 +346,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
       bool blocked = false;
       for (int j = 0; j < op.k && !blocked; ++j)
         blocked = op.tgt[j] < p.T &&
-                  (block_all[op.tgt[j]] || (op.kind == OP_DENSE && block_dense[op.tgt[j]]));
+                  (block_all[op.tgt[j]] || (op.kind != OP_DIAG && block_dense[op.tgt[j]]));
       bool take = false;
       if (!blocked) {
         if (op.kind == OP_DIAG) {
@@ -345,8 +471,15 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
           for (int j = 0; j < kx; ++j) old |= ((int(nidx) >> (kr + kt + j)) & 1) << extb[j].second;
           ro.coeff[nidx] = op.coeff[old];
         }
+      } else if (op.kind == OP_PERM) {
+        const int rc = reg_of(op.tgt[0]), rt = reg_of(op.tgt[1]);
+        if (rc < 0 || rt < 0) return false;
+        ro.mask = (1 << rc) | (1 << rt);
+        ro.src[0] = rc;
+        ro.src[1] = rt;
       } else {
         int ri[kMaxK];
+        ro.stype = op.stype;
         for (int j = 0; j < op.k; ++j) {
           ri[j] = reg_of(op.tgt[j]);
           if (ri[j] < 0) return false;  // cannot happen by construction
@@ -1387,7 +1520,14 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     };
     std::vector<KernelOp> ops;
     bool merge = !opt.no_diag_merge;
-    if (merge) {
+    // c128, on request (no_factor == -1): fused 2q gates as D P (A x B) when
+    // that has fewer FMAs (see factor_2q).  Off by default: width-2 fusion of
+    // layered circuits also absorbs the NEXT layer's 1q gates, (A' x B') D P
+    // (A x B), so only ~1/6 of the gates factor, and the extra ops / diagonal
+    // tables made layered-30 c128 slower (374 vs 330 ms measured)
+    bool factor = prec == SVB_C128 && opt.no_factor == -1 && merge;
+    for (int attempt = 0; attempt < 2 && merge; ++attempt) {
+      ops.clear();
       DiagAcc acc;
       for (int gi : taken) {
         const Gate& g = gates[gi];
@@ -1396,15 +1536,49 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
         if (g.diag) {
           if (!acc.empty() && acc.union_size(tg, g.k) > kMaxDiagK) ops.push_back(acc.take());
           acc.absorb(tg, g.k, g.m, gi);
-        } else {
-          if (!acc.empty() && acc.touches(tg, g.k)) ops.push_back(acc.take());
-          ops.push_back(lower_plain(gi));
+          continue;
         }
+        Factor2q fz;
+        if (factor && g.k == 2 && factor_2q(g.m, fz) && factored_cost(fz) < 16.0) {
+          if (!acc.empty() && acc.touches(tg, g.k)) ops.push_back(acc.take());
+          for (int side = 0; side < 2; ++side) {
+            const bool id = side ? fz.b_id : fz.a_id;
+            if (id) continue;
+            KernelOp o;
+            o.kind = OP_DENSE;
+            o.k = 1;
+            o.tgt[0] = tg[side];
+            o.coeff = side ? fz.B : fz.A;
+            o.stype = side ? fz.b_st : fz.a_st;
+            o.gates.push_back(gi);
+            ops.push_back(o);
+          }
+          if (fz.perm) {
+            KernelOp o;
+            o.kind = OP_PERM;
+            o.k = 2;
+            o.tgt[0] = fz.perm == 1 ? tg[0] : tg[1];  // control
+            o.tgt[1] = fz.perm == 1 ? tg[1] : tg[0];  // target
+            o.gates.push_back(gi);
+            ops.push_back(o);
+          }
+          // D opens (or joins) a diagonal run
+          if (!acc.empty() && acc.union_size(tg, 2) > kMaxDiagK) ops.push_back(acc.take());
+          acc.absorb(tg, 2, fz.d, gi);
+          continue;
+        }
+        if (!acc.empty() && acc.touches(tg, g.k)) ops.push_back(acc.take());
+        ops.push_back(lower_plain(gi));
       }
       if (!acc.empty()) ops.push_back(acc.take());
       size_t used = 0;
       for (auto& o : ops) used += coeff_elems(o);
-      if (used > pool_cap) merge = false;  // merged tables grew past the pool
+      if (used <= pool_cap && int(ops.size()) <= kMaxOps) break;
+      if (factor) {
+        factor = false;  // factorised ops overflow the pass: retry plain
+        continue;
+      }
+      merge = false;  // merged tables grew past the pool
     }
     if (!merge) {
       ops.clear();

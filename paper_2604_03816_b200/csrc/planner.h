@@ -29,6 +29,7 @@ struct Gate {
 struct KernelOp {
   int kind = OP_DENSE;
   int k = 0;
+  int stype = 0;           // dense 1q: DenseStructure (OP_PERM: tgt[0] control, tgt[1] target)
   int tgt[kMaxK] = {0};    // tile-local bits, matrix-local bit j -> tgt[j]; diagonal ops
                            // only: tgt >= T is shard qubit tgt - T outside the tile
                            // (always the top table bits, ascending)
@@ -57,6 +58,7 @@ struct RegPhase {
 struct RegOp {
   int kind = OP_DENSE;
   int k = 0;
+  int stype = 0;           // dense 1q: DenseStructure
   int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
   int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
   unsigned char rmap[32] = {0};  // diagonal: register part of the table index per rho

@@ -192,6 +192,11 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
         d.rmask = ro.rmask;
         d.xmask = ro.xmask;
         if (ro.kx) a.h.has_outside = 1;
+      } else if (ro.kind == OP_PERM) {
+        d.srt[0] = ro.src[0];  // control register bit
+        d.srt[1] = ro.src[1];  // target register bit
+      } else {
+        d.kx = ro.stype;  // dense 1q column structure
       }
       for (const cd& z : ro.coeff) {
         a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
@@ -773,7 +778,12 @@ int svb_plan_pass_gates(const svb_plan* plan, int pass, int* out, int cap) {
   if (pass < 0 || pass >= int(plan->plan.passes.size())) return fail(SVB_EINVAL, "pass index out of range");
   int w = 0;
   const Pass& ps = plan->plan.passes[pass];
+  // a factorised gate (c128 D P (A x B)) is several kernel ops: listed once,
+  // at its first op (its ops follow every earlier gate's on shared qubits)
+  std::vector<int> seen;
   auto emit = [&](int g) {
+    if (std::find(seen.begin(), seen.end(), g) != seen.end()) return true;
+    seen.push_back(g);
     if (w >= cap) return false;
     out[w++] = g;
     return true;

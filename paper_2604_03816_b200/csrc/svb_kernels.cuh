@@ -242,11 +242,28 @@ __device__ __forceinline__ void tile_diag(C* __restrict__ buf, const OpDesc& op,
 
 // KMAX bounds the dense arity compiled into a kernel variant, so the common
 // (fused width <= 2) variant carries no register pressure from wide gates.
+// CNOT on tile bits tgt[0] (control) -> tgt[1] (target): swap pairs in place.
+template <class C>
+__device__ __forceinline__ void tile_perm(C* __restrict__ buf, const OpDesc& op, int T, int tid) {
+  const int c = op.tgt[0], t = op.tgt[1];
+  const int lo = c < t ? c : t, hi = c < t ? t : c;
+  for (int e = tid; e < (1 << (T - 2)); e += kComputeThreads) {
+    const int base = insert_zero(insert_zero(e, lo), hi) | (1 << c);
+    const C a = buf[base], b = buf[base | (1 << t)];
+    buf[base] = b;
+    buf[base | (1 << t)] = a;
+  }
+}
+
 template <class C, int KMAX>
 __device__ __forceinline__ void tile_apply(C* buf, const OpDesc& op, const C* pool, int T, int tid,
                                            long long origin) {
   if (op.kind == OP_DIAG) {
     tile_diag<C>(buf, op, pool, T, tid, origin);
+    return;
+  }
+  if (op.kind == OP_PERM) {
+    tile_perm<C>(buf, op, T, tid);
     return;
   }
   switch (op.k) {

@@ -91,7 +91,8 @@ OPTS = [{}, {"tile_bits": 6, "min_low_bits": 2}, {"tile_bits": 9, "min_low_bits"
         {"cost_budget": 6.0}, {"tensor_cores": -1, "no_window_search": 1},
         {"tensor_cores": 2}, {"tensor_cores": 2, "tc_min_dense": 1, "cost_budget": 20.0},
         {"tile_bits": 12}, {"tile_bits": 12, "stages": 2, "tensor_cores": -1},
-        {"tile_bits": 13}, {"tile_bits": 13, "tc_min_dense": 1}, {"streams": 2}, {"streams": 1}, {"streams": 3}, {"streams": 4}, {"streams": 2, "tile_bits": 12}]
+        {"tile_bits": 13}, {"tile_bits": 13, "tc_min_dense": 1}, {"streams": 2}, {"streams": 1}, {"streams": 3}, {"streams": 4}, {"streams": 2, "tile_bits": 12},
+        {"no_factor": -1}, {"gemm_warps": 8}, {"tensor_cores": 2}]
 
 
 @pytest.mark.parametrize("opts", OPTS, ids=[str(o) for o in OPTS])

@@ -47,6 +47,12 @@ def emulate(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                 if op["kind"] == "dense":
                     u = op["coeffs"].reshape(1 << op["k"], 1 << op["k"])
                     orc.apply_matrix(buf, T, op["targets"], u)
+                elif op["kind"] == "perm":  # CNOT(control, target) on tile bits
+                    c_, t_ = op["targets"]
+                    e = np.arange(1 << T)
+                    sel = ((e >> c_) & 1).astype(bool) & ~((e >> t_) & 1).astype(bool)
+                    a_, b_ = e[sel], e[sel] | (1 << t_)
+                    buf[a_], buf[b_] = buf[b_].copy(), buf[a_].copy()
                 else:
                     d = np.zeros(1 << T, dtype=np.int64)
                     e = np.arange(1 << T)
@@ -218,6 +224,12 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                             v[:] = v @ U.T
                         continue
                     op = ops[o]
+                    if op["kind"] == "perm":  # CNOT on register bits
+                        cm, tm = 1 << op["ctrl"], 1 << op["tgt"]
+                        for rho in range(nr):
+                            if rho & cm and not rho & tm:
+                                v[:, [rho, rho | tm]] = v[:, [rho | tm, rho]]
+                        continue
                     if op["kind"] == "dense":
                         k, mask = op["k"], op["mask"]
                         d = 1 << k
@@ -412,3 +424,32 @@ def test_gemm_plans_cover_diagonals_and_readouts():
             for f in range(info["num_phases"]):
                 layouts.add(bool(nat.phase(p, f)["flags"] & 8))
     assert with_ops > 0 and layouts == {False, True}
+
+
+FACTOR_CASES = [
+    ("layered14", lambda: fuse(gen.layered_circuit(14, layers=6, seed=3), 2)[0]),
+    ("layered13_w2b", lambda: fuse(gen.layered_circuit(13, layers=8, seed=8), 2)[0]),
+    ("qft13", lambda: fuse(gen.qft_circuit(13), 2)[0]),
+    ("mixed14", lambda: fuse(_mixed_circuit(14, 4, 6), 2)[0]),
+]
+
+
+@pytest.mark.parametrize("name,make", FACTOR_CASES, ids=[c[0] for c in FACTOR_CASES])
+def test_c128_factorised_gates(name, make):
+    """c128 plans factor fused 2q gates as D P (A x B) (1-qubit ops with real /
+    imaginary columns, a CNOT register permutation, the diagonal merged into a
+    run): register-phase and shared-memory lowering both emulated."""
+    c = make()
+    want = orc.run_circuit(c, "double")
+    plan = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates, plan_options(no_factor=-1))
+    kinds = [plan.native.kernel_op(p, i)["kind"] for p in range(plan.num_passes)
+             for i in range(plan.native.pass_info(p)["num_kernel_ops"])]
+    if name.startswith("layered"):
+        assert "perm" in kinds
+    assert np.abs(emulate_reg(plan, c.num_qubits, "double") - want).max() <= 1e-12
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+    tile = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates, plan_options(no_reg_phases=1, no_factor=-1))
+    assert np.abs(emulate(tile, c.num_qubits, "double") - want).max() <= 1e-12
+    plain = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates)  # default: dense
+    assert all(plain.native.kernel_op(p, i)["kind"] != "perm" for p in range(plain.num_passes)
+               for i in range(plain.native.pass_info(p)["num_kernel_ops"]))
