@@ -278,3 +278,43 @@ def test_layered28_c64_full_size_vs_oracle():
     want = oracle_run(f, "single")
     err, fid = check(got, want, "single", "layered-28 c64")
     print(f"layered-28 c64 full size: max-abs {err:.3e}, 1 - F {1 - fid:.3e}")
+
+
+def test_chunked_host_views_at_32q_bounded_rss():
+    """host views of a 32-qubit c64 state (32 GiB) through pinned,
+    double-buffered 1 GiB chunks -- resident memory grows by the result array
+    plus the two staging chunks, never by a second state-sized copy; the
+    probabilities come chunk by chunk (no 2^32-double device array)."""
+    import gc
+
+    import psutil
+    import torch
+    n = 32
+    eng = B200Engine("b200-views")
+    st = eng.init_state(n, Precision.SINGLE)
+    # a non-trivial state: H on the top qubit and a phase on qubit 3
+    eng.apply_gate(st, GateOp(GateKind.H, (n - 1,)))
+    eng.apply_gate(st, GateOp(GateKind.H, (3,)))
+    eng.apply_gate(st, GateOp(GateKind.RZ, (3,), (0.7,)))
+    proc = psutil.Process()
+    gc.collect()
+    rss0 = proc.memory_info().rss
+    amps = st.amplitudes
+    grown = proc.memory_info().rss - rss0
+    assert amps.nbytes == 8 << n
+    assert grown <= amps.nbytes + (3 << 30), grown
+    nz = np.flatnonzero(amps)
+    assert set(nz.tolist()) == {0, 8, 1 << (n - 1), (1 << (n - 1)) + 8}
+    assert np.allclose(np.abs(amps[nz]), 0.5, atol=1e-6)
+    del amps
+    st._host = None
+    gc.collect()
+    free0 = torch.cuda.mem_get_info()[0]
+    probs = eng.probabilities(st)
+    assert torch.cuda.mem_get_info()[0] >= free0 - (2 << 30)  # one chunk of device scratch
+    assert abs(float(probs.sum()) - 1.0) <= 1e-6 and probs.dtype == np.float64
+    del probs
+    eng.release(st)
+    del st
+    gc.collect()
+    torch.cuda.empty_cache()
