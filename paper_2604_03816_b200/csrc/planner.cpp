@@ -283,6 +283,10 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DIAG && op.k > kMaxK) return false;
+  // factorised c128 ops (CNOT permutations) run on the shared-memory kernel:
+  // register-kernel support cost ~10 % on every c128 pass (measured)
+  for (const KernelOp& op : p.ops)
+    if (op.kind == OP_PERM) return false;
   std::vector<int> pending(p.ops.size());
   for (size_t i = 0; i < p.ops.size(); ++i) pending[i] = int(i);
   std::vector<std::vector<int>> sets, members;

@@ -192,11 +192,6 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
         d.rmask = ro.rmask;
         d.xmask = ro.xmask;
         if (ro.kx) a.h.has_outside = 1;
-      } else if (ro.kind == OP_PERM) {
-        d.srt[0] = ro.src[0];  // control register bit
-        d.srt[1] = ro.src[1];  // target register bit
-      } else {
-        d.kx = ro.stype;  // dense 1q column structure
       }
       for (const cd& z : ro.coeff) {
         a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
@@ -406,7 +401,14 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
   while (a.h.stages > 2 && smem_of() > size_t(f->max_smem)) --a.h.stages;
   if (a.h.n_phases > 0 && a.h.thread_bits == 7) {  // stage s belongs to stream s % streams
     const int g = a.h.streams >= 3 ? a.h.streams : 2;
-    a.h.stages = a.h.streams >= 3 ? a.h.streams : std::max(g, a.h.stages / g * g);  // 3-4 streams: one stage each
+    // 3-4 producer-free streams: one stage each; SVB_REG_STAGES=2 gives each
+    // two (the next tile loads while this one computes) when shared memory
+    // allows
+    static const int per = [] {
+      const char* e = std::getenv("SVB_REG_STAGES");
+      return e ? std::max(1, std::min(2, std::atoi(e))) : 1;  // measured neutral (qft-30: 133 vs 132 ms)
+    }();
+    a.h.stages = a.h.streams >= 3 ? a.h.streams * per : std::max(g, a.h.stages / g * g);
     while (a.h.stages > g && smem_of() > size_t(f->max_smem)) a.h.stages -= g;
   }
   const size_t smem = smem_of();

@@ -138,91 +138,9 @@ __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, cons
   }
 }
 
-// 1-qubit op whose columns are each purely real or purely imaginary (the
-// planner's c128 factorisation of fused gates: H, RX after row-phase
-// normalisation): 2 multiplies + 2 FMAs per output amplitude instead of 4 FMAs
-// -- (a + ib) r = (ar, br); (a + ib)(i s) = (-bs, as).
-template <class C, int RB, int MASK, int ST>
-__device__ __forceinline__ void reg_dense1s(C (&v)[1 << RB], const C* __restrict__ Ms) {
-  constexpr bool c0r = ST == ST_RR || ST == ST_RI;  // column 0 real (else imaginary)
-  constexpr bool c1r = ST == ST_RR || ST == ST_IR;
-  const auto a00 = c0r ? Ms[0].x : Ms[0].y, a10 = c0r ? Ms[2].x : Ms[2].y;
-  const auto a01 = c1r ? Ms[1].x : Ms[1].y, a11 = c1r ? Ms[3].x : Ms[3].y;
-  constexpr int REST = ((1 << RB) - 1) & ~MASK;
-#pragma unroll
-  for (int g = 0; g < (1 << (RB - 1)); ++g) {
-    const int b0 = deposit_mask<RB>(g, REST), b1 = b0 | MASK;
-    const C x0 = v[b0], x1 = v[b1];
-    C y0, y1;
-    if constexpr (c0r) {
-      y0.x = a00 * x0.x, y0.y = a00 * x0.y;
-      y1.x = a10 * x0.x, y1.y = a10 * x0.y;
-    } else {
-      y0.x = -a00 * x0.y, y0.y = a00 * x0.x;
-      y1.x = -a10 * x0.y, y1.y = a10 * x0.x;
-    }
-    if constexpr (c1r) {
-      y0.x = fma(a01, x1.x, y0.x), y0.y = fma(a01, x1.y, y0.y);
-      y1.x = fma(a11, x1.x, y1.x), y1.y = fma(a11, x1.y, y1.y);
-    } else {
-      y0.x = fma(-a01, x1.y, y0.x), y0.y = fma(a01, x1.x, y0.y);
-      y1.x = fma(-a11, x1.y, y1.x), y1.y = fma(a11, x1.x, y1.y);
-    }
-    v[b0] = y0;
-    v[b1] = y1;
-  }
-}
-
-template <class C, int RB>
-__device__ __forceinline__ void reg_dense1s_op(C (&v)[1 << RB], int mask, int st, const C* co) {
-  switch (mask * 8 + st) {
-#define SVB_SCASE(b, t)                                                          \
-  case (1 << (b)) * 8 + (t):                                                     \
-    if constexpr ((b) < RB) reg_dense1s<C, RB, (1 << (b)), (t)>(v, co);          \
-    return;
-#define SVB_SCASES(b) SVB_SCASE(b, 1) SVB_SCASE(b, 2) SVB_SCASE(b, 3) SVB_SCASE(b, 4)
-    SVB_SCASES(0) SVB_SCASES(1) SVB_SCASES(2) SVB_SCASES(3) SVB_SCASES(4)
-#undef SVB_SCASES
-#undef SVB_SCASE
-    default: break;
-  }
-}
-
-// CNOT on register bits (control CB, target TT): swap v[rho] and v[rho ^ 2^TT]
-// where bit CB of rho is set -- register moves, no arithmetic.
-template <class C, int RB, int CB, int TT>
-__device__ __forceinline__ void reg_perm(C (&v)[1 << RB]) {
-#pragma unroll
-  for (int rho = 0; rho < (1 << RB); ++rho)
-    if (((rho >> CB) & 1) && !((rho >> TT) & 1)) {
-      const C t = v[rho];
-      v[rho] = v[rho | (1 << TT)];
-      v[rho | (1 << TT)] = t;
-    }
-}
-
-template <class C, int RB>
-__device__ __forceinline__ void reg_perm_op(C (&v)[1 << RB], const OpDesc& op) {
-  switch (op.srt[0] * 8 + op.srt[1]) {
-#define SVB_PCASE(c, t)                                                       \
-  case (c) * 8 + (t):                                                         \
-    if constexpr ((c) < RB && (t) < RB && (c) != (t)) reg_perm<C, RB, (c), (t)>(v); \
-    return;
-#define SVB_PROW(c) SVB_PCASE(c, 0) SVB_PCASE(c, 1) SVB_PCASE(c, 2) SVB_PCASE(c, 3) SVB_PCASE(c, 4)
-    SVB_PROW(0) SVB_PROW(1) SVB_PROW(2) SVB_PROW(3) SVB_PROW(4)
-#undef SVB_PROW
-#undef SVB_PCASE
-    default: break;
-  }
-}
-
 template <class C, int RB, bool HOIST = true>
 __device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool) {
   const C* co = pool + op.coeff_off;
-  if (op.kx != ST_GENERAL && (op.pad & (op.pad - 1)) == 0) {  // structured 1-qubit op
-    reg_dense1s_op<C, RB>(v, op.pad, op.kx, co);
-    return;
-  }
   switch (op.pad) {  // register-bit mask of the dense op
 #define SVB_CASE(m) \
   case m:           \
@@ -241,8 +159,6 @@ template <class C, int RB>
 __device__ __forceinline__ void reg_apply(C (&v)[1 << RB], const OpDesc& op, const C* pool, int dbase) {
   if (op.kind == OP_DIAG)
     reg_diag<C, RB>(v, op, pool + op.coeff_off, dbase);
-  else if (op.kind == OP_PERM)
-    reg_perm_op<C, RB>(v, op);
   else
     reg_dense_op<C, RB>(v, op, pool);
 }
@@ -810,8 +726,14 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
   // advanced incrementally (S is a multiple of NG)
   int s = group, xs = group, tpar = 0;
   uint32_t parity = 0;
-  if constexpr (kNP) {  // each stream owns stage `group`: load its first tile
-    if ((gt >> 5) == 0 && group < mine) stream_load(group, group, gt & 31);
+  // kNP: each stream owns the stages group, group + NG, ... (S / NG of them):
+  // its first S / NG tiles load at once, and each consumed stage is refilled
+  // with the tile S / NG iterations ahead (latency hidden behind that many
+  // tiles of work)
+  const int ahead = S;  // tiles (of this CTA) between a tile and its stage's next one
+  if constexpr (kNP) {
+    if ((gt >> 5) == 0)
+      for (int t = group; t < S && t < mine; t += NG) stream_load(t, t, gt & 31);
   }
   for (int it = group; it < mine; it += NG) {
     const int tile = int(blockIdx.x) + it * int(gridDim.x);
@@ -852,9 +774,9 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
         if constexpr (kNP) {
           // warp 0 of the stream refills the stage with the stream's next tile
           // as soon as every thread has read it (overlaps this last phase)
-          if ((gt >> 5) == 0 && it + NG < mine) {
+          if ((gt >> 5) == 0 && it + ahead < mine) {
             mbar_wait(&empty[s], parity);
-            stream_load(it + NG, s, gt & 31);
+            stream_load(it + ahead, s, gt & 31);
           }
         }
       }
@@ -876,8 +798,6 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
         if (op.kind == OP_DIAG)
           reg_diag<C, RB>(v, op, pool + op.coeff_off,
                           int(dthr[o * NTG + gt]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
-        else if (op.kind == OP_PERM)
-          reg_perm_op<C, RB>(v, op);
         else
           reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4)>(v, op, pool);
       }
@@ -928,9 +848,9 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
         for (int r = 0; r < NR; ++r) dst[lin_g.at(r)] = buf[Swz<C>::f(r * NTG + gt)];
         mbar_arrive(&empty[s]);
         if constexpr (kNP) {
-          if ((gt >> 5) == 0 && it + NG < mine) {
+          if ((gt >> 5) == 0 && it + ahead < mine) {
             mbar_wait(&empty[s], parity);
-            stream_load(it + NG, s, gt & 31);
+            stream_load(it + ahead, s, gt & 31);
           }
         }
       }

@@ -23,11 +23,12 @@ constexpr int kComputeWarps = 8;
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kThreads = kComputeThreads + 32;   // + one TMA producer warp
 
-// OP_PERM: a CNOT on tile bits (tgt[0] control, tgt[1] target) -- a register
-// permutation, no arithmetic (c128 planner factorisation of fused gates)
+// OP_PERM: a CNOT on tile bits (tgt[0] control, tgt[1] target): pairs of
+// amplitudes swapped, no arithmetic (the opt-in c128 factorisation of fused
+// gates; executed by the shared-memory kernel)
 enum OpKind : int { OP_DENSE = 0, OP_DIAG = 1, OP_PERM = 2 };
-// structure of a 1-qubit dense op's columns (cheaper FP64 application):
-// ST_GENERAL, or each column purely real / purely imaginary
+// structure of a 1-qubit dense op's columns (planner bookkeeping of the
+// factorisation): ST_GENERAL, or each column purely real / purely imaginary
 enum DenseStructure : int { ST_GENERAL = 0, ST_RR = 1, ST_RI = 2, ST_IR = 3, ST_II = 4 };
 
 struct OpDesc {
@@ -41,7 +42,7 @@ struct OpDesc {
   // the tile (ascending, mask xmask).  They are constant over a tile, so a
   // diagonal gate never needs its qubits in the tile: its factor for those
   // bits is selected per tile from the tile origin.
-  int kx;             // diagonal: outside-tile bits; dense 1q: DenseStructure
+  int kx;             // diagonal: outside-tile bits
   int rmask;          // diagonal (register phases): register indices read by the table
   unsigned long long xmask;
 };

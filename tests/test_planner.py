@@ -37,6 +37,13 @@ def emulate(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
     amps = orc.init_state(n, precision)
     nat = plan.native
     for p in range(nat.num_passes()):
+        emulate_tile_pass(amps, nat, p, n)
+    return amps
+
+
+def emulate_tile_pass(amps: np.ndarray, nat, p: int, n: int) -> None:
+    """One pass as k_tile_pass runs it (tile gather, ops on tile bits, scatter)."""
+    if True:
         info = nat.pass_info(p)
         T = info["tile_bits"]
         ops = [nat.kernel_op(p, i) for i in range(info["num_kernel_ops"])]
@@ -61,7 +68,6 @@ def emulate(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                         d |= (((e >> t) if t < T else (idx >> (t - T))) & 1) << b
                     buf *= op["coeffs"].astype(buf.dtype)[d]
             amps[idx] = buf
-    return amps
 
 
 def plan_order_state(plan: CircuitPlan, circuit, precision: str) -> np.ndarray:
@@ -173,6 +179,9 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
     for p in range(nat.num_passes()):
         info = nat.pass_info(p)
         T, rb = info["tile_bits"], info["reg_bits"]
+        if rb == 0 and info["kernel"] == "tile":  # a shared-memory pass inside a register plan
+            emulate_tile_pass(amps, nat, p, n)
+            continue
         assert rb > 0 and T - rb in (7, 8)
         nr = 1 << rb
         nthreads = 1 << (T - rb)
