@@ -1329,8 +1329,9 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   const int mmax = T - Lmin;
   const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
                           ? opt.max_ops_per_pass : kMaxOps;
-  const double budget =
+  const double default_budget =
       opt.cost_budget == 0.0 ? default_cost_budget(prec) : opt.cost_budget;
+  double budget = default_budget;  // the tail merge below lifts it
   const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
   const CostModel cm(prec);
 
@@ -1445,23 +1446,28 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     return r;
   };
 
-  while (!pending.empty()) {
-    // candidate passes: the unrestricted greedy scan, and one scan per window
-    // of consecutive strided qubits; keep the one absorbing the most gates
-    Scan best = scan(pending, nullptr);
+  // candidate passes: the unrestricted greedy scan, and one scan per window
+  // of consecutive strided qubits; keep the one absorbing the most gates
+  auto best_scan = [&](const std::vector<int>& pend) {
+    Scan best = scan(pend, nullptr);
     if (mmax > 0 && !opt.no_window_search) {
       std::vector<char> allowed(n, 0);
       for (int a = Lmin; a + mmax <= n; ++a) {
         std::fill(allowed.begin(), allowed.end(), 0);
         for (int q = a; q < a + mmax; ++q) allowed[q] = 1;
-        Scan cand = scan(pending, &allowed);
+        Scan cand = scan(pend, &allowed);
         if (cand.taken.size() > best.taken.size() ||
             (cand.taken.size() == best.taken.size() && cand.cost < best.cost))
           best = std::move(cand);
       }
     }
+    return best;
+  };
+  std::vector<std::vector<int>> taken_of;  // the gates of each emitted pass (circuit order)
+
+  // Lower one scan result to a pass and append it (false + err on failure)
+  auto emit = [&](Scan& best) -> bool {
     std::vector<int>& taken = best.taken;
-    std::vector<int>& deferred = best.deferred;
     std::vector<char>& in_high = best.in_high;
 
     // ---- tile qubit set: low Lmin qubits + chosen high ones, filled upward
@@ -1632,7 +1638,59 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     p.cost = 0.0;
     for (auto& o : p.ops) p.cost += o.kind == OP_DIAG ? cm.diag(o.k) : cm.dense(o.k);
     plan.passes.push_back(std::move(p));
-    pending.swap(deferred);
+    taken_of.push_back(taken);
+    return true;
+  };
+
+  while (!pending.empty()) {
+    Scan best = best_scan(pending);
+    if (!emit(best)) return false;
+    pending.swap(best.deferred);
+  }
+
+  // Tail merge: the greedy scan can leave a last pass with a handful of gates
+  // (QFT-30 c128 and layered-33 c128 ended with a one-gate pass -- a full HBM
+  // round trip for one gate).  Re-plan the gates of the last k passes with the
+  // cost budget lifted (the tile, op and coefficient limits still hold) and
+  // keep the result when it needs fewer than k passes.
+  for (int k = 2; k <= 4 && budget >= 0 && int(plan.passes.size()) >= k; ++k) {
+    const size_t P = plan.passes.size();
+    if (taken_of[P - 1].size() > taken_of[P - 2].size() / 2 + 2) break;  // no short tail
+    std::vector<int> tail;
+    for (size_t q = P - k; q < P; ++q) tail.insert(tail.end(), taken_of[q].begin(), taken_of[q].end());
+    std::sort(tail.begin(), tail.end());  // circuit order (every scan keeps circuit order)
+    budget = -1.0;
+    // the first re-planned pass tries every window (the most-gates choice is
+    // what left the tail), the rest are greedy
+    std::vector<Scan> re;
+    std::vector<char> allowed(n, 0);
+    for (int a = Lmin - 1; a + mmax <= n && re.empty(); ++a) {
+      if (a >= Lmin) {
+        std::fill(allowed.begin(), allowed.end(), 0);
+        for (int q = a; q < a + mmax; ++q) allowed[q] = 1;
+      } else if (mmax == 0 || opt.no_window_search) {
+        a = n;  // unrestricted only
+      }
+      std::vector<Scan> cand{scan(tail, a >= Lmin && a < n ? &allowed : nullptr)};
+      while (!cand.back().deferred.empty() && int(cand.size()) < k - 1) cand.push_back(best_scan(cand.back().deferred));
+      if (cand.back().deferred.empty()) re = std::move(cand);
+    }
+    budget = default_budget;
+    if (re.empty()) continue;
+    std::vector<Pass> keep(std::make_move_iterator(plan.passes.end() - k), std::make_move_iterator(plan.passes.end()));
+    std::vector<std::vector<int>> keep_t(taken_of.end() - k, taken_of.end());
+    plan.passes.resize(P - k);
+    taken_of.resize(P - k);
+    bool ok = true;
+    for (Scan& sc : re) ok = ok && emit(sc);
+    if (!ok) {  // lowering refused a merged pass: restore the originals
+      plan.passes.resize(P - k);
+      taken_of.resize(P - k);
+      for (auto& x : keep) plan.passes.push_back(std::move(x));
+      for (auto& x : keep_t) taken_of.push_back(std::move(x));
+      err.clear();
+    }
+    break;
   }
   return true;
 }

@@ -531,6 +531,21 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
     if (in > 0.0 && out > 0.0) corr = float(sqrt(in / out));
   }
   double acc_in = 0.0, acc_out = 0.0;  // this thread's norm^2 contributions (true units)
+  // Scale factor: when the previous pass of this execution was a GEMM pass,
+  // its output norm^2 is the state's norm^2, so one power of two for the whole
+  // pass bounds every amplitude (|amp| S < 2^15): no per-tile norm reduction.
+  // fp16 hi/lo then carries ~2^-22 of the STATE norm per element (absolute),
+  // instead of 2^-22 of each tile's norm.  Otherwise (first pass) the scale
+  // comes from each tile's 2-norm.
+  float Sg = 0.f;
+  if (h.normacc && h.pass_index > 0 && !(h.debug & 512)) {
+    const double prev = h.normacc[2 * h.pass_index - 1];
+    if (prev > 0.0) {
+      const int ebits = (__float_as_int(sqrtf(float(prev))) >> 23) & 0xff;
+      Sg = __int_as_float(min(max(268 - ebits, 1), 253) << 23);
+      if (blockIdx.x == 0 && tid == 0) acc_in = prev * double(corr) * double(corr);
+    }
+  }
   // stage timestamps (SVB_GEMM_TRACE): CTA 0, stream 0, thread 0, first 8 tiles x 16 events
   unsigned long long* tr = (h.trace && blockIdx.x == 0 && group == 0 && gt == 0) ? h.trace : nullptr;
   int tev = 0;
@@ -595,22 +610,26 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
           }
         }
       }
-      {
+      if (Sg > 0.f) {
+        group_bar<NG, NTG>(group);  // every read of the linear tile done (A is written in place)
+        mark(it);                   // 2: loaded
+        S = Sg;
+      } else {
         float w = 0.f;
 #pragma unroll
         for (int k = 0; k < NH; ++k) w += norm2_chains(v[k]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
         if (lane == 0) red[group * 16 + wig] = w;
+        group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
+        mark(it);  // 2: loaded + norm
+        n2in = sum_red(0);
+        // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
+        const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
+        const int se = min(max(268 - ebits, 1), 253);
+        S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
+        if (gt == 0) acc_in += double(n2in) * double(corr) * double(corr);
       }
-      group_bar<NG, NTG>(group);  // every read of the linear tile done; partials visible
-      mark(it);  // 2: loaded + norm
-      n2in = sum_red(0);
-      // S = 2^(14 - e), e = exponent of the tile 2-norm: |amp| S < 2^15 for the pass
-      const int ebits = (__float_as_int(sqrtf(n2in)) >> 23) & 0xff;
-      const int se = min(max(268 - ebits, 1), 253);
-      S = n2in > 0.f ? __int_as_float(se << 23) : 1.f;
-      if (gt == 0) acc_in += double(n2in) * double(corr) * double(corr);
       const float Sc = S * corr;
       const uint32_t wb0 = tab.wb[0][gt7];
 #pragma unroll
