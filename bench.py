@@ -662,14 +662,16 @@ def run_sharded(args, eng, fused, circuit, n, precision, cfg, kind, rank, world,
                        "norm_after": float(nt.item())},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_reg_pass (local passes)",
+                         "kernel": "local passes (k_gemm_pass / k_reg_pass); swaps: k_swap over CUDA-IPC peer memory"
+                                   if sh._use_p2p(backend.tensor(state)) else "local passes; swaps: NCCL send/recv",
                          "nvlink": {"bytes_sent_per_gpu": sent, "achieved_gbs": nvl,
                                     "peak_gbs": nvl_peak,
                                     "peak_kind": "measured: 1 GiB pairwise send/recv, max over ranks",
                                     "frac": (nvl / nvl_peak) if (nvl and nvl_peak) else None}},
             "e2e": {"value": g0 / statistics.median(e2e), "unit": "gates/s",
                     "h2d_bytes_per_step": n_passes * PASS_ARGS_BYTES, "d2h_bytes_per_step": 8},
-            "gpu_launches": args.steps * (n_passes + 2),
+            # passes + the |0> fill (2 kernels) + one swap kernel per swap (p2p)
+            "gpu_launches": args.steps * (n_passes + 2 + (len(swaps) if sh._use_p2p(backend.tensor(state)) else 0)),
             "clocks": clk.summary(),
             "cpu_baseline": None,
         }

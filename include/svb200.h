@@ -186,6 +186,25 @@ int svb_block_sums(const void* amps, int n_local, int prec, int log_block, doubl
 int svb_sample_search(const void* amps, int n_local, int prec, int log_block, const double* block_cum,
                       const double* targets, long long shots, long long* out_indices, void* stream);
 
+/* Global-qubit swap between shards -- replaces nothing in the reference (which
+ * has no multi-device path); it is the exchange step of the north star's
+ * sharding.  Swaps two equal byte ranges in place in ONE
+ * kernel: each 16-byte element pair is read and written by one thread, so no
+ * staging buffer and no second copy.  `a` and `b` may live on different GPUs
+ * (peer access enabled with svb_enable_peer_access, or a peer buffer mapped
+ * with svb_ipc_import): the loads/stores of the remote side travel over
+ * NVLink.  The kernel runs on the current device's `stream`; bytes % 16 == 0. */
+int svb_swap_blocks(void* a, void* b, long long bytes, void* stream);
+/* cudaDeviceEnablePeerAccess(peer) from `device` (already-enabled is OK). */
+int svb_enable_peer_access(int device, int peer);
+/* CUDA IPC of a device buffer between the processes of one node (torchrun
+ * ranks): export writes a 64-byte handle of the allocation holding `ptr` and
+ * ptr's offset in it; import maps a peer's allocation into this process and
+ * returns ptr (base + offset) and the base to close later. */
+int svb_ipc_export(const void* ptr, void* handle64, long long* offset);
+int svb_ipc_import(const void* handle64, long long offset, void** ptr, void** base);
+int svb_ipc_close(void* base);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,8 @@ EXPORTS = (
     "svb_plan_phase_tc", "svb_plan_tc_matrix", "svb_plan_phase_op_ext", "svb_plan_phase_map",
     "svb_plan_execute",
     "svb_plan_execute_range", "svb_plan_destroy", "svb_dot", "svb_dot_mixed", "svb_norm2",
-    "svb_probabilities", "svb_block_sums", "svb_sample_search",
+    "svb_probabilities", "svb_block_sums", "svb_sample_search", "svb_swap_blocks",
+    "svb_enable_peer_access", "svb_ipc_export", "svb_ipc_import", "svb_ipc_close",
 )
 
 
@@ -99,6 +100,11 @@ def lib():
         "svb_probabilities": (i, [vp, i, ll, ll, vp, vp]),
         "svb_block_sums": (i, [vp, i, i, i, vp, vp]),
         "svb_sample_search": (i, [vp, i, i, i, vp, vp, ll, vp, vp]),
+        "svb_swap_blocks": (i, [vp, vp, ll, vp]),
+        "svb_enable_peer_access": (i, [i, i]),
+        "svb_ipc_export": (i, [vp, vp, C.POINTER(C.c_longlong)]),
+        "svb_ipc_import": (i, [vp, ll, C.POINTER(vp), C.POINTER(vp)]),
+        "svb_ipc_close": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -230,3 +236,32 @@ class NativePlan:
             self.close()
         except Exception:  # pragma: no cover - interpreter shutdown
             pass
+
+
+def swap_blocks(a_ptr: int, b_ptr: int, nbytes: int, stream: int) -> None:
+    """In-place a <-> b of two device ranges in one kernel (svb_swap_blocks)."""
+    check(lib().svb_swap_blocks(C.c_void_p(a_ptr), C.c_void_p(b_ptr), int(nbytes), C.c_void_p(stream)))
+
+
+def enable_peer_access(device: int, peer: int) -> None:
+    check(lib().svb_enable_peer_access(int(device), int(peer)))
+
+
+def ipc_export(ptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding ptr, ptr's offset in it)."""
+    h = (C.c_ubyte * 64)()
+    off = C.c_longlong()
+    check(lib().svb_ipc_export(C.c_void_p(ptr), h, C.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def ipc_import(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map a peer process's allocation: (pointer, base to pass to ipc_close)."""
+    h = (C.c_ubyte * 64).from_buffer_copy(handle)
+    ptr, base = C.c_void_p(), C.c_void_p()
+    check(lib().svb_ipc_import(h, int(offset), C.byref(ptr), C.byref(base)))
+    return int(ptr.value), int(base.value)
+
+
+def ipc_close(base: int) -> None:
+    check(lib().svb_ipc_close(C.c_void_p(base)))

@@ -944,4 +944,84 @@ int svb_probabilities(const void* amps, int prec, long long offset, long long co
   return SVB_OK;
 }
 
+int svb_swap_blocks(void* a, void* b, long long bytes, void* stream) {
+  if (!a || !b) return fail(SVB_EINVAL, "null argument");
+  if (bytes < 0 || (bytes & 15) || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+    return fail(SVB_EINVAL, "swap ranges must be 16-byte aligned multiples of 16 bytes");
+  if (bytes == 0) return SVB_OK;
+  DeviceFacts* f = nullptr;
+  int rc = device_facts(&f);
+  if (rc) return rc;
+  const long long n = bytes / 16;
+  const int threads = 512;
+  // 4 CTAs of 512 per SM, each thread 4 pairs in flight: ~64 KB of remote
+  // loads outstanding per SM
+  long long grid = std::min<long long>((n + 4LL * threads - 1) / (4LL * threads), (long long)f->sm_count * 4);
+  if (grid < 1) grid = 1;
+  k_swap<4><<<unsigned(grid), threads, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint4*>(a),
+                                                                            static_cast<uint4*>(b), n);
+  SVB_CUDA(cudaGetLastError());
+  return SVB_OK;
+}
+
+int svb_enable_peer_access(int device, int peer) {
+  int cur = 0;
+  SVB_CUDA(cudaGetDevice(&cur));
+  if (device == peer) return SVB_OK;
+  int can = 0;
+  SVB_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return fail(SVB_EUNSUPPORTED, "no peer access between these devices");
+  SVB_CUDA(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(SVB_ECUDA, cudaGetErrorString(e));
+  return SVB_OK;
+}
+
+int svb_ipc_export(const void* ptr, void* handle64, long long* offset) {
+  if (!ptr || !handle64 || !offset) return fail(SVB_EINVAL, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  // driver entry point fetched at run time: the library must load on hosts
+  // without libcuda (the CPU test-suite)
+  static PFN_cuMemGetAddressRange_v3020 range_fn = [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    return cudaGetDriverEntryPoint("cuMemGetAddressRange", &q, cudaEnableDefault, &r) == cudaSuccess &&
+                   r == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(q)
+               : nullptr;
+  }();
+  if (!range_fn) return fail(SVB_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(SVB_EINVAL, "pointer is not a device allocation");
+  cudaIpcMemHandle_t h;
+  SVB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle64, &h, 64);
+  *offset = static_cast<long long>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return SVB_OK;
+}
+
+int svb_ipc_import(const void* handle64, long long offset, void** ptr, void** base) {
+  if (!handle64 || !ptr || !base || offset < 0) return fail(SVB_EINVAL, "bad argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  void* b = nullptr;
+  SVB_CUDA(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = b;
+  *ptr = static_cast<char*>(b) + offset;
+  return SVB_OK;
+}
+
+int svb_ipc_close(void* base) {
+  if (!base) return fail(SVB_EINVAL, "null argument");
+  SVB_CUDA(cudaIpcCloseMemHandle(base));
+  return SVB_OK;
+}
+
 }  // extern "C"

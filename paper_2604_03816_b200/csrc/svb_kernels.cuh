@@ -397,6 +397,34 @@ __global__ void k_set_one(C* amps, long long one) {
 
 // <a|b> partial sums in FP64; a and b may differ in precision (both are
 // promoted to complex128 first, as ref engines.py:340-346 promotes states)
+// In-place swap of two equal ranges (global-qubit exchange between shards):
+// each 16-byte pair is loaded and stored by one thread, either side may be a
+// peer GPU's memory (NVLink loads/stores).  Four independent pairs per thread
+// per iteration keep enough remote loads in flight to cover NVLink latency.
+template <int U = 4>
+__global__ void __launch_bounds__(512) k_swap(uint4* __restrict__ a, uint4* __restrict__ b, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    uint4 x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u] = a[i + u * stride];
+      y[u] = b[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[i + u * stride] = y[u];
+      b[i + u * stride] = x[u];
+    }
+  }
+  for (; i < n; i += stride) {
+    const uint4 x = a[i], y = b[i];
+    a[i] = y;
+    b[i] = x;
+  }
+}
+
 template <class CA, class CB = CA>
 __global__ void k_dot(const CA* __restrict__ a, const CB* __restrict__ b, long long n, double2* __restrict__ partial) {
   double re = 0.0, im = 0.0;

@@ -12,9 +12,9 @@ the same call: ``aqsim.run_circuit("b200", circuit)`` on 34-36 qubits gives a
   gates restricted to a shard's global bits are those of ``sharded.py``
   (``schedule`` / ``localize``), shared with the torchrun engine.
 * Local segments run as native plans on every shard's device (async, one
-  stream per device); a swap exchanges blocks between shards device to
-  device (peer copies over NVLink between GPUs), chunked through a staging
-  buffer.
+  stream per device); a swap exchanges blocks between shards in place with
+  one kernel per device (svb_swap_blocks: loads and stores of the peer's
+  half over NVLink, no staging buffer).
 * Host views (``amplitudes``, ``probabilities``) and sampling first restore
   the identity layout on the device (``canonicalize``: physical SWAP gates
   on local qubits, block exchanges for global ones, a shard relabelling for
@@ -26,9 +26,6 @@ import numpy as np
 
 from .circuit import Circuit, GateKind, GateOp, as_precision
 from .sharded import LocalStep, SwapStep, _schedule_once, block_peer, localize, own_block, schedule
-
-STAGING_ELEMS = 1 << 24
-
 
 class ShardedDeviceState:
     """A 2^n state sharded over the devices of this process (see module doc)."""
@@ -128,26 +125,25 @@ def _run_local(state: ShardedDeviceState, gates) -> None:
         eng.execute(sh, eng.plan(Circuit(nl, mine), state.precision))
 
 
-def _swap_blocks(a, b, staging) -> None:
-    """a <-> b (equal-length 1-D tensors, possibly on different devices)."""
-    step = staging.numel()
-    for c0 in range(0, a.numel(), step):
-        c1 = min(a.numel(), c0 + step)
-        tmp = staging[:c1 - c0]
-        tmp.copy_(a[c0:c1])
-        a[c0:c1].copy_(b[c0:c1])
-        b[c0:c1].copy_(tmp)
-
-
 def exchange(state: ShardedDeviceState, step: SwapStep) -> None:
     """Swap the step's global qubits with the top m local qubits: shard r's
     block own(p) <-> shard p's block own(r) for every partner p (the same
-    pairing as the NCCL path, sharded.ShardedEngine.exchange)."""
+    pairing as the torchrun path, sharded.ShardedEngine.exchange).
+
+    Each pair of blocks is swapped IN PLACE by the swap kernel
+    (svb_swap_blocks): shard r's device swaps the first half of the pair and
+    shard p's device the second half, concurrently, each reading and writing
+    the other GPU's half through peer access (NVLink) -- no staging buffer,
+    no extra device copy, both link directions busy."""
     import torch
+
+    from . import _native
     state.synchronize()
     nl = step.n_local
     blk = 1 << (nl - step.m)
+    esz = state.shards[0].tensor.element_size()
     done = set()
+    used = set()
     for r in range(state.world):
         for w in range(1 << step.m):
             if w == own_block(r, step):
@@ -158,10 +154,27 @@ def exchange(state: ShardedDeviceState, step: SwapStep) -> None:
             done.add((min(r, p), max(r, p)))
             ta, tb = state.shards[r].tensor, state.shards[p].tensor
             wa, wb = own_block(p, step), own_block(r, step)
-            with torch.cuda.device(ta.device):
-                staging = torch.empty(min(blk, STAGING_ELEMS), dtype=ta.dtype, device=ta.device)
-                _swap_blocks(ta[wa * blk:(wa + 1) * blk], tb[wb * blk:(wb + 1) * blk], staging)
-    for dev in {s.tensor.device for s in state.shards}:
+            a0 = ta.data_ptr() + wa * blk * esz
+            b0 = tb.data_ptr() + wb * blk * esz
+            total = blk * esz
+            if total % 16:  # a single c64 amplitude per block (tiny states)
+                sa, sb = ta[wa * blk:(wa + 1) * blk], tb[wb * blk:(wb + 1) * blk]
+                tmp = sa.clone()
+                sa.copy_(sb.to(sa.device))
+                sb.copy_(tmp.to(sb.device))
+                used.update((ta.device, tb.device))
+                continue
+            half = (total // 2) // 16 * 16
+            for dev, lo, hi in ((ta.device, 0, half), (tb.device, half, total)):
+                if hi <= lo:
+                    continue
+                if ta.device != tb.device:
+                    other = tb.device if dev == ta.device else ta.device
+                    _native.enable_peer_access(dev.index, other.index)
+                with torch.cuda.device(dev):
+                    _native.swap_blocks(a0 + lo, b0 + lo, hi - lo, torch.cuda.current_stream(dev).cuda_stream)
+                used.add(dev)
+    for dev in used:
         torch.cuda.synchronize(dev)
     for s in state.shards:
         s.touch()

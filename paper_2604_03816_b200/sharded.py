@@ -24,9 +24,15 @@ ref ``circuit.py:189-194``):
   the preceding segment, and the *initial* layout is chosen so that the first
   swap needs none (|0...0> is invariant under qubit relabelling).
 
-Transport is ``torch.distributed`` point-to-point (NCCL over NVLink on the
-GPU box, gloo in the CPU tests), chunked through a double-buffered staging
-area so the copy-back of chunk c overlaps the transfer of chunk c+1.
+Transport on the GPU box (``p2p``, the default for CUDA shards): every rank
+maps its peers' shards into its address space once (CUDA IPC handles
+exchanged over ``torch.distributed``) and a swap is ONE kernel per rank
+(``svb_swap_blocks``): for each block pair the lower rank swaps the first
+half and the higher rank the second half, loading and storing the peer's
+memory over NVLink -- in place, no staging buffer, no copy-back.  The
+fallback (``p2p=False``, and the CPU tests) is ``torch.distributed``
+point-to-point chunked through a double-buffered staging area so that the
+copy-back of chunk c overlaps the transfer of chunk c+1.
 """
 from __future__ import annotations
 
@@ -287,7 +293,7 @@ class CudaShardBackend:
 class ShardedEngine:
     """Runs circuits on a state sharded over the torch.distributed world."""
 
-    def __init__(self, backend, group=None, chunk_elems: int = 1 << 24):
+    def __init__(self, backend, group=None, chunk_elems: int = 1 << 24, p2p: bool | None = None):
         import torch.distributed as dist
         self.dist = dist
         self.backend = backend
@@ -296,6 +302,72 @@ class ShardedEngine:
         self.world = dist.get_world_size(group)
         self.chunk_elems = chunk_elems
         self._staging = None
+        # None: peer-mapped swap kernel when the shards are CUDA tensors under
+        # NCCL (one node); True forces it (e.g. gloo ranks sharing one GPU)
+        self.p2p = p2p
+        self._peers = {}   # peer allocation's IPC handle -> mapped base
+        self._bases = []   # IPC mappings to close
+
+    def close(self) -> None:
+        from . import _native
+        for b in self._bases:
+            try:
+                _native.ipc_close(b)
+            except Exception:  # pragma: no cover - teardown
+                pass
+        self._bases = []
+        self._peers = {}
+
+    def _use_p2p(self, t) -> bool:
+        if not t.is_cuda:
+            return False
+        if self.p2p is not None:
+            return bool(self.p2p)
+        return self.dist.get_backend(self.group) == "nccl"
+
+    def _peer_ptrs(self, t) -> dict:
+        """Every rank's shard mapped into this process (CUDA IPC).  Handles
+        are gathered at every exchange (a re-allocated shard gets a new
+        handle even at a recycled address); mappings are cached per handle."""
+        from . import _native
+        mine = _native.ipc_export(t.data_ptr())
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        ptrs = {}
+        for r, (h, off) in enumerate(allh):
+            if r == self.rank:
+                ptrs[r] = t.data_ptr()
+                continue
+            if h not in self._peers:
+                _ptr, base = _native.ipc_import(h, 0)
+                self._peers[h] = base
+                self._bases.append(base)
+            ptrs[r] = self._peers[h] + off
+        return ptrs
+
+    def _exchange_p2p_step(self, t, step, blk: int, peers) -> None:
+        """Block swaps as one kernel per rank over peer-mapped memory: the pair
+        (our block w, peer's block own(rank)) is split in halves, the lower
+        rank swaps the first, the higher the second, both at once."""
+        import torch
+
+        from . import _native
+        ptrs = self._peer_ptrs(t)
+        esz = t.element_size()
+        total = blk * esz
+        half = (total // 2) // 16 * 16
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+        torch.cuda.synchronize(t.device)    # this shard's earlier passes are done ...
+        self.dist.barrier(group=self.group)  # ... and every peer's
+        mine = own_block(self.rank, step)   # where our block w lands on the peer
+        for w, peer in peers:
+            a0 = t.data_ptr() + w * total
+            b0 = ptrs[peer] + mine * total
+            lo, hi = (0, half) if self.rank < peer else (half, total)
+            if hi > lo:
+                _native.swap_blocks(a0 + lo, b0 + lo, hi - lo, stream)
+        torch.cuda.synchronize(t.device)    # our half of every pair is swapped ...
+        self.dist.barrier(group=self.group)  # ... and the peers' halves
 
     # -------------------------------------------------------------- program
     def compile(self, circuit, precision=Precision.DOUBLE):
@@ -351,6 +423,11 @@ class ShardedEngine:
         if not peers:
             return
         npeer = len(peers)
+        if self._use_p2p(t) and (blk * t.element_size()) % 16 == 0:
+            self._exchange_p2p_step(t, step, blk, peers)
+            if hasattr(state, "touch"):
+                state.touch()
+            return
         if t.is_cuda and dist.get_backend(self.group) == "gloo":
             # gloo moves host tensors only (used by the single-GPU multi-process
             # tests): stage each block through host memory

@@ -333,9 +333,11 @@ def test_cli_run_and_bench_scaling(capsys):
     assert rows[0]["fused_time_s"] > 0
 
 
-def _sharded_cuda_worker(rank, world, port, out):
+def _sharded_cuda_worker(rank, world, port, out, p2p=False):
     """One rank of the sharded engine on cuda:0 with its CUDA local plans;
-    exchanges over gloo through host memory (one GPU on this box)."""
+    exchanges over gloo through host memory (one GPU on this box), or with
+    p2p the swap kernel on CUDA-IPC-mapped peer shards (gloo only carries the
+    handles and the barriers)."""
     import os
     import torch.distributed as dist
     from paper_2604_03816_b200.sharded import CudaShardBackend, ShardedEngine
@@ -346,7 +348,7 @@ def _sharded_cuda_worker(rank, world, port, out):
         errs = []
         for c, prec in ((fuse(gen.layered_circuit(16, layers=6, seed=4), 2)[0], "single"),
                         (fuse(gen.qft_circuit(15), 2)[0], "double")):
-            eng = ShardedEngine(CudaShardBackend(0))
+            eng = ShardedEngine(CudaShardBackend(0), p2p=p2p)
             st = eng.run_circuit(c, Precision(prec))
             full = st.gather()
             norm = st.norm_squared()
@@ -354,14 +356,17 @@ def _sharded_cuda_worker(rank, world, port, out):
                 want = orc.run_circuit(c, prec)
                 errs += [float(np.abs(full.astype(np.complex128) - want.astype(np.complex128)).max()),
                          abs(norm - 1), st.schedule.num_swaps()]
+            if p2p:
+                errs.append(float(len(eng._bases)))  # peer shards were IPC-mapped
+            eng.close()
         if rank == 0:
             np.save(out, np.array(errs))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_engine_on_device(world):
+@pytest.mark.parametrize("world,p2p", [(2, False), (4, False), (2, True), (4, True)])
+def test_sharded_engine_on_device(world, p2p):
     """The multi-GPU engine end to end with the CUDA backend: `world` ranks
     share cuda:0, local segments run the native plans (including diagonal
     gates restricted to each rank's global bits), swaps over gloo."""
@@ -374,7 +379,12 @@ def test_sharded_engine_on_device(world):
         port = sk.getsockname()[1]
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "res.npy")
-        mp.spawn(_sharded_cuda_worker, args=(world, port, out), nprocs=world, join=True)
-        e64, n64, s64, e128, n128, s128 = np.load(out)
+        mp.spawn(_sharded_cuda_worker, args=(world, port, out, p2p), nprocs=world, join=True)
+        res = np.load(out)
+    if p2p:
+        e64, n64, s64, m64, e128, n128, s128, m128 = res
+        assert m64 == world - 1 and m128 == world - 1
+    else:
+        e64, n64, s64, e128, n128, s128 = res
     assert e64 <= 1e-5 and n64 <= 1e-5 and s64 >= 1
     assert e128 <= 1e-12 and n128 <= 1e-10 and s128 >= 1
