@@ -1326,7 +1326,15 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
   if (Lmin > T) Lmin = T;
   if (Lmin < T - kMaxHigh) Lmin = T - kMaxHigh;
   if (prec == SVB_C64 && Lmin < 1) Lmin = 1;  // chunks must be >= 16 bytes
-  const int mmax = T - Lmin;
+  int mmax = T - Lmin;
+  // Wide-chunk alternative (1 KiB contiguous runs: 7 low bits c64, 6 c128):
+  // a pass whose strided tile qubits are scattered reads 2^L-amplitude chunks
+  // all over the shard, and at 128 B (the default L) HBM runs at 20-50 % of
+  // its bandwidth (measured on random-target circuits, paper Table 2: n = 30
+  // c64 69 -> 47 ms, c128 432 -> 302 ms with 1 KiB chunks).  Used for a pass
+  // when it absorbs >= 90 % of the gates the default candidate does.
+  const int Lbase = Lmin;
+  const int Lwide = opt.min_low_bits > 0 ? Lbase : std::min(T - 2, prec == SVB_C64 ? 7 : 6);
   const int max_ops = (opt.max_ops_per_pass > 0 && opt.max_ops_per_pass < kMaxOps)
                           ? opt.max_ops_per_pass : kMaxOps;
   const double default_budget =
@@ -1642,9 +1650,35 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
     return true;
   };
 
+  // runs of consecutive strided qubits a scan chose (a window search result
+  // is one run; scattered random targets give many)
+  auto high_runs = [&](const Scan& sc) {
+    int runs = 0;
+    for (int q = Lbase; q < n; ++q)
+      runs += sc.in_high[q] && (q == Lbase || !sc.in_high[q - 1]);
+    return runs;
+  };
   while (!pending.empty()) {
     Scan best = best_scan(pending);
-    if (!emit(best)) return false;
+    if (Lwide > Lbase) {
+      Lmin = Lwide;
+      mmax = T - Lmin;
+      Scan wide = best_scan(pending);
+      // scattered strided qubits (> 2 runs) cost 3-7x the HBM time at 128-B
+      // chunks (measured): the wide candidate wins at >= 60 % of the gates;
+      // window-shaped candidates keep the default unless it is >= 90 %
+      const size_t need = high_runs(best) > 2 ? 6 : 9;
+      if (!wide.taken.empty() && wide.taken.size() * 10 >= best.taken.size() * need)
+        best = std::move(wide);
+      else {
+        Lmin = Lbase;
+        mmax = T - Lmin;
+      }
+    }
+    const bool ok = emit(best);
+    Lmin = Lbase;
+    mmax = T - Lmin;
+    if (!ok) return false;
     pending.swap(best.deferred);
   }
 

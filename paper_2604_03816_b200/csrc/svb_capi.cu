@@ -340,6 +340,13 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
         a.h.gemm_bufs = ng + 1;
         if (gemm_smem_layout(a.h, ng, f->dyn_smem_base).total > size_t(f->max_smem)) a.h.gemm_bufs = ng;
       }
+      // a pass whose coefficient pool and GEMM matrices leave no room for four
+      // tile buffers runs with three (then two) tile streams
+      while (wpg == 4 && ng > 2 && gemm_smem_layout(a.h, ng, f->dyn_smem_base).total > size_t(f->max_smem)) {
+        ng = ng == 5 ? 4 : ng - 1;
+        a.h.gemm_bufs = ng;
+        gfn = ng == 4 ? k_gemm_pass<4, 4, false> : ng == 3 ? k_gemm_pass<3, 4, true> : k_gemm_pass<2, 4, true>;
+      }
       const size_t smem_g = gemm_smem_layout(a.h, ng, f->dyn_smem_base).total;
       if (smem_g > size_t(f->max_smem)) return fail(SVB_EUNSUPPORTED, "gemm pass exceeds shared memory");
       long long grid = std::min<long long>(a.h.n_tiles, (long long)f->sm_count);

@@ -104,6 +104,37 @@ __device__ __forceinline__ void t5_mma_ss(uint32_t d, uint64_t a, uint64_t b, ui
       : "memory");
 }
 
+// The 12 MMAs of one GEMM (Ah Bh, Al Bh, Ah Bl; 4 K-steps each) in one asm
+// block from two base descriptors: every other descriptor is a small
+// constant added to the base's start-address field (A: +2 per 32-B K-step,
+// +1024 for A_lo 16 KB on; B: +16 per 256-B K-step, +512 for Bl 8 KB on; the
+// 14-bit field cannot carry: shared addresses < 256 KB).  Generated code
+// otherwise rebuilt and re-broadcast both 64-bit descriptors per MMA (~18
+// instructions each, serialised in the issuing thread on the tile's chain).
+__device__ __forceinline__ void gemm_issue12(uint32_t d, uint64_t ad, uint64_t bd) {
+  asm volatile(
+      "{\n .reg .pred pf, pt;\n .reg .b64 a0, a1, a2, a3, l0, l1, l2, l3, b0, b1, b2, b3, c0, c1, c2, c3;\n"
+      " setp.ne.b32 pf, %0, %0;\n setp.eq.b32 pt, %0, %0;\n"
+      " mov.b64 a0, %1;\n add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      " add.s64 l0, %1, 1024;\n add.s64 l1, %1, 1026;\n add.s64 l2, %1, 1028;\n add.s64 l3, %1, 1030;\n"
+      " mov.b64 b0, %2;\n add.s64 b1, %2, 16;\n add.s64 b2, %2, 32;\n add.s64 b3, %2, 48;\n"
+      " add.s64 c0, %2, 512;\n add.s64 c1, %2, 528;\n add.s64 c2, %2, 544;\n add.s64 c3, %2, 560;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %3, pf;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], l0, b0, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], l1, b1, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], l2, b2, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], l3, b3, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a0, c0, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a1, c1, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a2, c2, %3, pt;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], a3, c3, %3, pt;\n}" ::"r"(d),
+      "l"(ad), "l"(bd), "r"(kIdescN64)
+      : "memory");
+}
+
 // GEMM-completion wait: plain try_wait polling (no suspend hint: the GEMM takes
 // a few hundred cycles, a suspended warp may wake later than that), bounded
 // by %globaltimer like mbar_wait_bounded
@@ -650,10 +681,15 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
     for (int p = 1; p <= P; ++p) {
       const PhaseDesc& ph = args.phases[p];
       const bool ld16 = ph.flags & PH_LD16;
+      // warp-uniform copies (redux results live in uniform registers): the
+      // issuing thread then hands the descriptors to the tensor core without
+      // a per-MMA ELECT / R2UR.BROADCAST loop
+      const uint32_t abase_u = __reduce_or_sync(0xffffffffu, abase);
+      const uint32_t dacc_u = __reduce_or_sync(0xffffffffu, tbase + uint32_t(group) * kColsPerGroup);
       if (gt == 0) {
         t5_fence_after();
         const uint32_t b0 = mats + uint32_t(ph.tc) * kMmaMatBytes;
-        const uint32_t dacc = tbase + uint32_t(group) * kColsPerGroup;
+        const uint32_t dacc = dacc_u;
         if (!(h.debug & 1)) {
           if constexpr (N128) {
             // Ah [Bh | Bl] (N 128: the packed B is exactly the N = 128 K-major
@@ -666,7 +702,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
             for (int ks = 0; ks < 4; ++ks)
               t5_mma_ss(dacc, sw128_desc(abase + uint32_t(kGemmAWords * 4) + 32u * ks),
                         t5_desc(b0 + 256u * ks, 128, 1024), 1u, kIdescN64);
-          } else {
+          } else if (h.debug & 8192) {  // per-MMA descriptors (the previous issue code, for comparison)
 #pragma unroll
             for (int t = 0; t < 3; ++t)
 #pragma unroll
@@ -675,6 +711,8 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
                 const uint64_t bd = t5_desc(b0 + (t == 2 ? 8192u : 0u) + 256u * ks, 128, 1024);
                 t5_mma_ss(dacc, ad, bd, (t | ks) ? 1u : 0u);
               }
+          } else {
+            gemm_issue12(dacc, sw128_desc(abase_u), t5_desc(b0, 128, 1024));
           }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
