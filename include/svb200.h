@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SVB_ABI_VERSION 1
+#define SVB_ABI_VERSION 2
 #define SVB_MAX_TARGETS 8   /* per gate; ref allows any k, fusion emits k <= 3 */
 
 enum svb_precision { SVB_C64 = 0, SVB_C128 = 1 };
@@ -73,6 +73,9 @@ typedef struct svb_plan_options {
   int gemm_warps;       /* k_gemm_pass warps per tile stream: 4 or 8 (0: default 4) */
   int no_factor;        /* c128: -1 = factor fused 2q gates as D P (A x B) where cheaper
                            (structured 1q ops + CNOT permutation); 0/1 = keep them dense */
+  int no_gate_merge;    /* 1: keep every input gate a separate op (default: a dense gate
+                           is multiplied into the previous dense gate on the same <= 2
+                           qubits when nothing in between touches them) */
 } svb_plan_options;
 
 /* Per-pass description (for tests, profiling and the sharded driver). */

@@ -109,6 +109,28 @@ def cmd_bench_scaling(args) -> int:
     return 0
 
 
+def cmd_noise_compare(args) -> int:
+    """Exact outcome fidelity / TVD of depolarized Bell / GHZ circuits vs the
+    ideal state (ref cli.py:384-417), density matrices evolved on the device
+    (paper_2604_03816_b200.noise); JSON rows, exact columns only."""
+    from . import noise
+    eng = B200Engine("b200-cli")
+    rows = []
+    for width in (int(x) for x in args.widths.split(",") if x):
+        circuit = gen.ghz_circuit(width)
+        st = eng.run_circuit(circuit, Precision.DOUBLE)
+        probs = st.probabilities()
+        eng.release(st)
+        ideal = {format(i, f"0{width}b"): float(q) for i, q in enumerate(probs)}
+        for p in (float(x) for x in args.p_values.split(",") if x):
+            rho = noise.evolve_noisy(circuit, p, engine=eng)
+            f_cl, tvd = noise.metrics(noise.measure_distribution(rho), ideal)
+            rows.append({"circuit": circuit.name, "width": width, "p": p,
+                         "f_cl_exact": round(f_cl, 6), "tvd_exact": round(tvd, 6)})
+    sys.stdout.write(json.dumps(rows, indent=2, sort_keys=True) + "\n")
+    return 0
+
+
 def cmd_bench_fusion(args) -> int:
     """Depth reduction and time of each circuit unfused vs fused (ref
     cli.py:340-381; JSON rows instead of the reference's table)."""
@@ -158,6 +180,9 @@ def main(argv=None) -> int:
     b.add_argument("--repetitions", type=int, default=3)
     b.add_argument("--seed", type=int, default=0)
     b.add_argument("--no-timing", action="store_true")
+    nz = sub.add_parser("noise-compare")
+    nz.add_argument("--widths", default="2,3,4,5")
+    nz.add_argument("--p-values", default="0.0,0.001,0.01")
     f = sub.add_parser("bench-fusion")
     f.add_argument("--circuits", default="qft-12,ghz-12,random-12")
     f.add_argument("--fuse-width", type=int, default=2)
@@ -167,7 +192,8 @@ def main(argv=None) -> int:
     f.add_argument("--no-timing", action="store_true")
     args = ap.parse_args(argv)
     try:
-        return {"run": cmd_run, "bench-scaling": cmd_bench_scaling, "bench-fusion": cmd_bench_fusion}[args.cmd](args)
+        return {"run": cmd_run, "bench-scaling": cmd_bench_scaling, "bench-fusion": cmd_bench_fusion,
+                "noise-compare": cmd_noise_compare}[args.cmd](args)
     except ValueError as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 2

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libs
 SVB_C64, SVB_C128 = 0, 1
 SVB_OK, SVB_EINVAL, SVB_ECUDA, SVB_ENOMEM, SVB_EUNSUPPORTED = 0, -1, -2, -3, -4
 SVB_MAX_TARGETS = 8
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # every symbol declared in include/svb200.h (tests check the library exports them)
 EXPORTS = (
@@ -37,7 +37,7 @@ class PlanOptions(C.Structure):
                 ("no_diag_merge", C.c_int), ("stages", C.c_int), ("reg_bits", C.c_int),
                 ("no_reg_phases", C.c_int), ("tensor_cores", C.c_int), ("tc_min_dense", C.c_int),
                 ("no_window_search", C.c_int), ("streams", C.c_int), ("gemm_warps", C.c_int),
-                ("no_factor", C.c_int)]
+                ("no_factor", C.c_int), ("no_gate_merge", C.c_int)]
 
 
 class PassInfo(C.Structure):

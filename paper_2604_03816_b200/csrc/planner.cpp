@@ -1292,8 +1292,8 @@ bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const 
   return true;
 }
 
-bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_options& opt_in,
-                Plan& plan, std::string& err) {
+bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const svb_plan_options& opt_in,
+                       Plan& plan, std::string& err) {
   if (n < 1 || n > 62) {
     err = "n_local must be in 1..62";
     return false;
@@ -1665,9 +1665,9 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       mmax = T - Lmin;
       Scan wide = best_scan(pending);
       // scattered strided qubits (> 2 runs) cost 3-7x the HBM time at 128-B
-      // chunks (measured): the wide candidate wins at >= 60 % of the gates;
+      // chunks (measured): the wide candidate wins at >= 40 % of the gates;
       // window-shaped candidates keep the default unless it is >= 90 %
-      const size_t need = high_runs(best) > 2 ? 6 : 9;
+      const size_t need = high_runs(best) > 2 ? 4 : 9;
       if (!wide.taken.empty() && wide.taken.size() * 10 >= best.taken.size() * need)
         best = std::move(wide);
       else {
@@ -1725,6 +1725,146 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates, const svb_plan_
       err.clear();
     }
     break;
+  }
+  return true;
+}
+
+
+// ---- peephole gate merge (before pass building)
+// Unfused input (the paper's Table-2 circuits: 10n random single-qubit gates,
+// run gate by gate by the reference's bench-scaling, ref cli.py:304-337) has
+// runs of dense gates on the same qubits.  Each dense gate is multiplied into
+// the previous dense gate when that gate is the last one on all of its qubits
+// and the union stays <= 2 qubits; a 2-qubit gate also absorbs open 1-qubit
+// gates on its qubits.  Diagonal gates are never merge targets (a dense
+// factor would make a CP gate need both qubits in the tile).  The product is
+// the same operator up to rounding (~1e-16 per merge).
+namespace {
+// g's matrix acting on the qubit list tgt (g.t a subset of tgt), local bit j <-> tgt[j]
+std::vector<cd> expand_on(const Gate& g, const int* tgt, int k) {
+  const int D = 1 << k, d = 1 << g.k;
+  int pos[kMaxK];
+  for (int j = 0; j < g.k; ++j)
+    for (int i = 0; i < k; ++i)
+      if (tgt[i] == g.t[j]) pos[j] = i;
+  int gmask = 0;
+  for (int j = 0; j < g.k; ++j) gmask |= 1 << pos[j];
+  std::vector<cd> m(size_t(D) * D, cd());
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) {
+      if ((r & ~gmask) != (c & ~gmask)) continue;
+      int a = 0, b = 0;
+      for (int j = 0; j < g.k; ++j) {
+        a |= ((r >> pos[j]) & 1) << j;
+        b |= ((c >> pos[j]) & 1) << j;
+      }
+      m[size_t(r) * D + c] = g.diag ? (a == b ? g.m[a] : cd()) : g.m[size_t(a) * d + b];
+    }
+  return m;
+}
+std::vector<cd> matmul(const std::vector<cd>& x, const std::vector<cd>& y, int D) {
+  std::vector<cd> z(size_t(D) * D, cd());
+  for (int r = 0; r < D; ++r)
+    for (int q = 0; q < D; ++q) {
+      const cd a = x[size_t(r) * D + q];
+      if (a == cd()) continue;
+      for (int c = 0; c < D; ++c) z[size_t(r) * D + c] += a * y[size_t(q) * D + c];
+    }
+  return z;
+}
+}  // namespace
+
+std::vector<Gate> merge_gates(const std::vector<Gate>& in, int n, std::vector<std::vector<int>>& orig) {
+  std::vector<Gate> out;
+  std::vector<char> dead;
+  orig.clear();
+  std::vector<int> last(n, -1);  // qubit -> index in `out` of the last gate touching it
+  for (size_t i = 0; i < in.size(); ++i) {
+    const Gate& g = in[i];
+    if (!g.diag && g.k <= 2) {
+      const int c = last[g.t[0]];
+      bool same = c >= 0 && !out[c].diag;
+      for (int j = 1; j < g.k; ++j) same = same && last[g.t[j]] == c;
+      if (same) {  // every qubit of g: last touched by the dense gate c
+        Gate& h = out[c];
+        bool sub = true;  // g's qubits within h's
+        for (int j = 0; j < g.k; ++j) sub = sub && std::find(h.t, h.t + h.k, g.t[j]) != h.t + h.k;
+        if (sub) {
+          h.m = matmul(expand_on(g, h.t, h.k), h.m, 1 << h.k);
+          orig[c].push_back(int(i));
+          continue;
+        }
+      }
+      if (g.k == 2) {  // absorb open 1q gates on g's qubits
+        Gate ng = g;
+        std::vector<int> src;
+        for (int j = 0; j < 2; ++j) {
+          const int c1 = last[g.t[j]];
+          if (c1 >= 0 && !out[c1].diag && out[c1].k == 1) {
+            ng.m = matmul(ng.m, expand_on(out[c1], g.t, 2), 4);
+            dead[c1] = 1;
+            src.insert(src.end(), orig[c1].begin(), orig[c1].end());
+          }
+        }
+        if (!src.empty()) {
+          std::sort(src.begin(), src.end());
+          src.push_back(int(i));
+          out.push_back(ng);
+          dead.push_back(0);
+          orig.push_back(src);
+          for (int j = 0; j < 2; ++j) last[g.t[j]] = int(out.size()) - 1;
+          continue;
+        }
+      }
+    }
+    out.push_back(g);
+    dead.push_back(0);
+    orig.push_back({int(i)});
+    for (int j = 0; j < g.k; ++j) last[g.t[j]] = int(out.size()) - 1;
+  }
+  std::vector<Gate> res;
+  std::vector<std::vector<int>> ores;
+  for (size_t i = 0; i < out.size(); ++i)
+    if (!dead[i]) {
+      res.push_back(std::move(out[i]));
+      ores.push_back(std::move(orig[i]));
+    }
+  orig.swap(ores);
+  return res;
+}
+
+bool build_plan(int n, int prec, const std::vector<Gate>& gates_in, const svb_plan_options& opt_in,
+                Plan& plan, std::string& err) {
+  std::vector<std::vector<int>> orig;
+  std::vector<Gate> merged;
+  if (!opt_in.no_gate_merge) merged = merge_gates(gates_in, n, orig);
+  const std::vector<Gate>& gates = opt_in.no_gate_merge ? gates_in : merged;
+  if (!build_plan_merged(n, prec, gates, opt_in, plan, err)) return false;
+  if (opt_in.no_gate_merge) return true;
+  // input-gate indices everywhere (pass_gates, reports, tests)
+  auto remap = [&](std::vector<int>& v) {
+    std::vector<int> r;
+    for (int g : v) r.insert(r.end(), orig[g].begin(), orig[g].end());
+    std::sort(r.begin(), r.end());
+    v.swap(r);
+  };
+  for (Pass& p : plan.passes) {
+    int ng = 0;
+    std::vector<int> seen;
+    auto note = [&](const std::vector<int>& v) {
+      for (int g : v)
+        if (std::find(seen.begin(), seen.end(), g) == seen.end()) seen.push_back(g);
+    };
+    for (KernelOp& op : p.ops) {
+      note(op.gates);
+      remap(op.gates);
+    }
+    for (RegPhase& ph : p.phases) {
+      note(ph.tc_gates);
+      remap(ph.tc_gates);
+    }
+    for (int g : seen) ng += int(orig[g].size());
+    p.num_gates = ng;
   }
   return true;
 }

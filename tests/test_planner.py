@@ -462,3 +462,27 @@ def test_c128_factorised_gates(name, make):
     plain = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates)  # default: dense
     assert all(plain.native.kernel_op(p, i)["kind"] != "perm" for p in range(plain.num_passes)
                for i in range(plain.native.pass_info(p)["num_kernel_ops"]))
+
+
+def test_gate_merge_of_unfused_runs():
+    """Unfused input (the paper's Table-2 circuits): runs of dense gates on the
+    same qubits become one op; pass_gates still lists every input gate, and
+    the state equals the oracle's and the unmerged plan's."""
+    c = gen.random_su2_circuit(10, 100, seed=3)
+    want = orc.run_circuit(c, "double")
+    o = dict(tensor_cores=-1, tile_bits=8, min_low_bits=2)
+    merged = CircuitPlan(10, Precision.DOUBLE, c.gates, plan_options(**o))
+    plain = CircuitPlan(10, Precision.DOUBLE, c.gates, plan_options(no_gate_merge=1, **o))
+    n_ops = [sum(p.native.pass_info(i)["num_kernel_ops"] for i in range(p.num_passes)) for p in (merged, plain)]
+    assert n_ops[0] < n_ops[1] and n_ops[1] >= 100
+    assert sum(i["num_gates"] for i in merged.passes()) == len(c.gates)
+    for p in (merged, plain):
+        assert np.abs(plan_order_state(p, c, "double") - want).max() <= 1e-12
+        assert np.abs(emulate(p, 10, "double") - want).max() <= 1e-12
+    # a 2q gate absorbs the open 1q gates on its qubits; a diagonal gate blocks a merge
+    g = [GateOp(GateKind.H, (0,)), GateOp(GateKind.RX, (1,), (0.3,)), GateOp(GateKind.CNOT, (0, 1)),
+         GateOp(GateKind.RZ, (1,), (0.7,)), GateOp(GateKind.RY, (1,), (0.2,)), GateOp(GateKind.H, (0,))]
+    c2 = Circuit(4, g)
+    p2 = CircuitPlan(4, Precision.DOUBLE, g, plan_options(tensor_cores=-1, tile_bits=4, min_low_bits=1))
+    assert np.abs(emulate(p2, 4, "double") - orc.run_circuit(c2, "double")).max() <= 1e-12
+    assert sum(i["num_kernel_ops"] for i in p2.passes()) < len(g)
