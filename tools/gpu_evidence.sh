@@ -3,6 +3,7 @@
 # baseline), the reference arm, the ncu launch list of one config-2 step and
 # full captures of the dominant kernels (c64 gemm pass, c128 register pass).
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_noise.py -m gpu -q > gpurun_out/pytest_noise.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_noise.txt
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
 timeout 900 python bench.py > gpurun_out/bench_default.txt 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.txt 2>&1
