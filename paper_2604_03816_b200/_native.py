@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsvb200.so")
+# SVB_LIB: load another build of the library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("SVB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libsvb200.so")
 
 SVB_C64, SVB_C128 = 0, 1
 SVB_OK, SVB_EINVAL, SVB_ECUDA, SVB_ENOMEM, SVB_EUNSUPPORTED = 0, -1, -2, -3, -4

@@ -287,6 +287,11 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   if (p.T != RB + TB) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DENSE && op.k > std::min(RB, 3)) return false;
+  // the c128 stream kernels carry no 3-qubit dense code (op-dispatch size,
+  // see reg_dense_op): such passes take the 8-thread-bit kernel
+  if (prec == SVB_C128 && TB == 7)
+    for (const KernelOp& op : p.ops)
+      if (op.kind == OP_DENSE && op.k > 2) return false;
   for (const KernelOp& op : p.ops)
     if (op.kind == OP_DIAG && op.k > kMaxK) return false;
   // factorised c128 ops (CNOT permutations) run on the shared-memory kernel:

@@ -94,6 +94,7 @@ int device_facts(DeviceFacts** out) {
                          (const void*)k_reg_pass<float2, 5, 7>, (const void*)k_reg_pass<double2, 4, 7>,
                          (const void*)k_reg_pass<float2, 5, 7, 3>, (const void*)k_reg_pass<double2, 4, 7, 3>,
                          (const void*)k_reg_pass<double2, 4, 7, 4>,
+                         (const void*)k_reg_pass<double2, 4, 7, 3, 1>, (const void*)k_reg_pass<double2, 4, 7, 3, 2>,
                          (const void*)k_reg_pass<float2, 5, 7, 4>,
                          (const void*)k_reg_pass<double2, 3>,  (const void*)k_reg_pass<double2, 4>};
     for (const void* fn : fns)
@@ -185,6 +186,21 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       d.k = ro.k;
       d.coeff_off = off;
       d.pad = ro.mask;
+      if (ro.kind == OP_DENSE && ro.k == 2 && ro.coeff.size() == 16 && !std::getenv("SVB_NO_SPARSE2")) {
+        // sparse 2q pattern from the exact zeros (register-local order; see
+        // reg_sparse2): monomial forms first, they also fit the 2-column ones
+        static const int order[6] = {5, 6, 1, 2, 3, 4};
+        for (int pat : order) {
+          bool ok = true;
+          for (int r = 0; r < 4 && ok; ++r)
+            for (int c = 0; c < 4 && ok; ++c)
+              if (c != sp_c1(pat, r) && c != sp_c2(pat, r)) ok = ro.coeff[size_t(r) * 4 + c] == cd();
+          if (ok) {
+            d.kx = pat;
+            break;
+          }
+        }
+      }
       if (ro.kind == OP_DIAG) {
         std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
@@ -370,8 +386,13 @@ int launch_pass(PassArgs<C>& a, int n_local, C* amps, cudaStream_t stream) {
     } else {
       if (a.h.reg_bits < 3 || a.h.reg_bits > 4 || (a.h.thread_bits == 7 && a.h.reg_bits != 4))
         return fail(SVB_EUNSUPPORTED, "c128 reg_bits must be 3..4 (two streams: 4)");
+      // sparse 2q patterns (OpDesc.kx, fill_args): the three-stream kernel
+      // with only the controlled-U forms unless the pass holds others
+      int sp = 0;
+      for (int i = 0; i < a.h.n_ops; ++i)
+        if (a.ops[i].kind == OP_DENSE && a.ops[i].k == 2) sp = std::max(sp, a.ops[i].kx == 0 ? 0 : a.ops[i].kx <= 2 ? 1 : 2);
       fn = a.h.thread_bits == 7 ? (a.h.streams == 4   ? k_reg_pass<C, 4, 7, 4>
-                                   : a.h.streams == 3 ? k_reg_pass<C, 4, 7, 3>
+                                   : a.h.streams == 3 ? (sp == 2 ? k_reg_pass<C, 4, 7, 3, 2> : k_reg_pass<C, 4, 7, 3, 1>)
                                                       : k_reg_pass<C, 4, 7>)
            : a.h.reg_bits == 4  ? k_reg_pass<C, 4>
                                 : k_reg_pass<C, 3>;

@@ -21,6 +21,8 @@ extern template __global__ void k_reg_pass<double2, 3>(double2*, const __grid_co
 extern template __global__ void k_reg_pass<double2, 4>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_reg_pass<double2, 4, 7>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_reg_pass<double2, 4, 7, 3>(double2*, const __grid_constant__ PassArgs<double2>);
+extern template __global__ void k_reg_pass<double2, 4, 7, 3, 1>(double2*, const __grid_constant__ PassArgs<double2>);
+extern template __global__ void k_reg_pass<double2, 4, 7, 3, 2>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_reg_pass<double2, 4, 7, 4>(double2*, const __grid_constant__ PassArgs<double2>);
 extern template __global__ void k_gemm_pass<4, 4, true>(float2*, const __grid_constant__ PassArgs<float2>);
 extern template __global__ void k_gemm_pass<4, 4, false>(float2*, const __grid_constant__ PassArgs<float2>);

@@ -138,13 +138,81 @@ __device__ __forceinline__ void reg_diag(C (&v)[1 << RB], const OpDesc& op, cons
   }
 }
 
-template <class C, int RB, bool HOIST = true>
+// Sparse 2-qubit ops (OpDesc.kx = pattern, set at launch from the exact zeros
+// of the 4x4 matrix in register-local order, index = b0 + 2 b1): every row
+// has 2 non-zero columns c1(i), c2(i) (controlled-U forms, CNOT-permuted
+// controlled forms) or 1 (CNOT permutation with phases).  Width-2 fusion of
+// CNOT layers leaves ~60 % of the fused 2q gates of a layered circuit in one
+// of these forms, and QFT's fused H . CP gates are controlled-U: half (or a
+// quarter) of the FP64 FMAs of a dense 4x4.
+//   1: rows keep b0, mix b1      c = {i & 1, (i & 1) | 2}
+//   2: rows keep b1, mix b0      c = {i & 2, (i & 2) | 1}
+//   3: rows 0,1 <- {0,3}, rows 2,3 <- {1,2}
+//   4: rows 0,2 <- {0,3}, rows 1,3 <- {1,2}
+//   5: monomial, 1 <-> 3          c = {0, 3, 2, 1}
+//   6: monomial, 2 <-> 3          c = {0, 1, 3, 2}
+__host__ __device__ constexpr int sp_c1(int pat, int i) {
+  return pat == 1 ? (i & 1) : pat == 2 ? (i & 2) : pat == 3 ? (i < 2 ? 0 : 1) : pat == 4 ? ((i & 1) ? 1 : 0)
+       : pat == 5 ? ((i & 1) ? (i ^ 2) : i) : ((i & 2) ? (i ^ 1) : i);
+}
+__host__ __device__ constexpr int sp_c2(int pat, int i) {
+  return pat == 1 ? ((i & 1) | 2) : pat == 2 ? ((i & 2) | 1) : pat == 3 ? (i < 2 ? 3 : 2)
+       : pat == 4 ? ((i & 1) ? 2 : 3) : -1;
+}
+template <class C, int RB, int MASK, int PAT, bool HOIST>
+__device__ __forceinline__ void reg_sparse2(C (&v)[1 << RB], const C* __restrict__ Ms) {
+  constexpr int REST = ((1 << RB) - 1) & ~MASK;
+  constexpr bool two = PAT <= 4;
+  C M1[4], M2[two ? 4 : 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    M1[i] = Ms[i * 4 + sp_c1(PAT, i)];
+    if constexpr (two) M2[i] = Ms[i * 4 + sp_c2(PAT, i)];
+  }
+#pragma unroll
+  for (int g = 0; g < (1 << (RB - 2)); ++g) {
+    const int base = deposit_mask<RB>(g, REST);
+    C in[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) in[j] = v[base | deposit_mask<RB>(j, MASK)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      C acc = cfma(M1[i], in[sp_c1(PAT, i)], czero<C>());
+      if constexpr (two) acc = cfma(M2[i], in[sp_c2(PAT, i)], acc);
+      v[base | deposit_mask<RB>(i, MASK)] = acc;
+    }
+  }
+}
+// SP: sparse patterns compiled in (0 none, 1 controlled-U forms 1-2, 2 all).
+// Every variant is unrolled code for each register mask, and the size of the
+// op dispatch matters (measured, qft-30 / layered-30 c128 ms: none 121 / 330,
+// SP 1 106 / 325, SP 2 111 / 314 -- both without 3-qubit dense ops): the
+// launch picks SP 2 only for passes holding patterns 3-6.
+template <class C, int RB, int MASK, bool HOIST, int SP>
+__device__ __forceinline__ void reg_dense2(C (&v)[1 << RB], const C* __restrict__ co, int pat) {
+  if constexpr (SP >= 1) {
+    if (pat == 1) return reg_sparse2<C, RB, MASK, 1, HOIST>(v, co);
+    if (pat == 2) return reg_sparse2<C, RB, MASK, 2, HOIST>(v, co);
+  }
+  if constexpr (SP >= 2) {
+    if (pat == 3) return reg_sparse2<C, RB, MASK, 3, HOIST>(v, co);
+    if (pat == 4) return reg_sparse2<C, RB, MASK, 4, HOIST>(v, co);
+    if (pat == 5) return reg_sparse2<C, RB, MASK, 5, HOIST>(v, co);
+    if (pat == 6) return reg_sparse2<C, RB, MASK, 6, HOIST>(v, co);
+  }
+  reg_dense<C, RB, MASK, HOIST>(v, co);
+}
+
+// D3: 3-qubit dense ops compiled in (the c128 stream kernels leave them to
+// the 8-thread-bit kernel: less code in the op dispatch)
+template <class C, int RB, bool HOIST = true, int SP = 0, bool D3 = true>
 __device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool) {
   const C* co = pool + op.coeff_off;
   switch (op.pad) {  // register-bit mask of the dense op
 #define SVB_CASE(m) \
   case m:           \
-    if constexpr ((m) < (1 << RB) && popc_c(m) <= 3) reg_dense<C, RB, (m), HOIST>(v, co); \
+    if constexpr ((m) < (1 << RB) && popc_c(m) == 2) reg_dense2<C, RB, (m), HOIST, SP>(v, co, op.kx); \
+    else if constexpr ((m) < (1 << RB) && popc_c(m) <= (D3 ? 3 : 2)) reg_dense<C, RB, (m), HOIST>(v, co); \
     break;
     SVB_CASE(1) SVB_CASE(2) SVB_CASE(3) SVB_CASE(4) SVB_CASE(5) SVB_CASE(6) SVB_CASE(7)
     SVB_CASE(8) SVB_CASE(9) SVB_CASE(10) SVB_CASE(11) SVB_CASE(12) SVB_CASE(13) SVB_CASE(14)
@@ -541,7 +609,7 @@ constexpr int reg_block_threads() {
 
 // NGRP: tile streams (0 = fill 256 compute threads); 3 streams of 128 threads
 // (c64 tcgen05 phases) make a 416-thread CTA.
-template <class C, int RB, int TB = 8, int NGRP = 0>
+template <class C, int RB, int TB = 8, int NGRP = 0, int SP = 0>
 __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 16 ? RB >= 4 : RB >= 5) ? 1 : 2)
     k_reg_pass(C* __restrict__ amps, const __grid_constant__ PassArgs<C> args) {
   constexpr int T = RB + TB;
@@ -799,7 +867,7 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
           reg_diag<C, RB>(v, op, pool + op.coeff_off,
                           int(dthr[o * NTG + gt]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
         else
-          reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4)>(v, op, pool);
+          reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4), SP, !(sizeof(C) == 16 && TB == 7)>(v, op, pool);
       }
       if constexpr (sizeof(C) == 8 && RB == 5) {
         if (last && h.renorm) {
