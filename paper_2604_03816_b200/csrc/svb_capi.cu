@@ -558,7 +558,9 @@ int exec_range(svb_plan* p, std::vector<PassArgs<C>>& args, void* amps, int firs
   if constexpr (sizeof(C) == 8) {
     bool any = false;
     for (const Pass& ps : p->plan.passes) any = any || ps.gemm;
-    if (any) {
+    // SVB_NO_RENORM=1: no deferred renormalisation (and a per-tile scale in
+    // every pass) -- exposes the raw fp16-split / fp32-accumulation error
+    if (any && !std::getenv("SVB_NO_RENORM")) {
       int dev = 0;
       SVB_CUDA(cudaGetDevice(&dev));
       double*& buf = p->normacc[{dev, s}];

@@ -318,3 +318,34 @@ def test_chunked_host_views_at_32q_bounded_rss():
     del st
     gc.collect()
     torch.cuda.empty_cache()
+
+
+def test_c64_tensor_core_error_without_renormalisation(multi_circuits, monkeypatch):
+    """ADVICE (round 1): measure the fp16 hi/lo split + fp32 tensor-core
+    accumulation error with the deferred renormalisation OFF (SVB_NO_RENORM=1:
+    no norm correction, per-tile scale in every pass), so the correction does
+    not mask it.  23 q layered c64 on the default k_gemm_pass plans: the raw
+    error stays inside the c64 tolerance, and the norm drift it leaves
+    (what the renormalisation removes) is bounded and reported."""
+    lay = multi_circuits["layered"]
+    want = oracle_run(lay, "single", key=("layered", "single"))
+    eng = B200Engine("b200-norenorm")
+    monkeypatch.setenv("SVB_NO_RENORM", "1")
+    st, plan = run_planned(eng, lay, "single")
+    assert any(i["kernel"] == "gemm" for i in plan.passes())
+    raw = st.amplitudes.astype(np.complex128)
+    eng.release(st)
+    monkeypatch.delenv("SVB_NO_RENORM")
+    st, _ = run_planned(eng, lay, "single")
+    ren = st.amplitudes.astype(np.complex128)
+    eng.release(st)
+    w = want.astype(np.complex128)
+    err_raw, err_ren = float(np.abs(raw - w).max()), float(np.abs(ren - w).max())
+    drift_raw = abs(float(np.vdot(raw, raw).real) - 1.0)
+    drift_ren = abs(float(np.vdot(ren, ren).real) - 1.0)
+    f_raw = float(abs(np.vdot(w, raw)) ** 2)  # un-normalised fidelity
+    print(f"layered-{N_MULTI} c64: max-abs raw {err_raw:.3e} / renormalised {err_ren:.3e}, "
+          f"|norm^2 - 1| raw {drift_raw:.3e} / renormalised {drift_ren:.3e}, raw F {f_raw:.8f}")
+    assert err_raw <= TOL["single"][0] and err_ren <= TOL["single"][0]
+    assert orc.normalised_fidelity(raw, w) >= 1 - TOL["single"][1]
+    assert drift_raw <= 1e-4 and drift_ren <= drift_raw + 1e-6
