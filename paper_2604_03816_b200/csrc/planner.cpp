@@ -1677,29 +1677,113 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
       runs += sc.in_high[q] && (q == Lbase || !sc.in_high[q - 1]);
     return runs;
   };
-  while (!pending.empty()) {
-    Scan best = best_scan(pending);
+  // The greedy step: the most-gates candidate, or its wide-chunk alternative.
+  // Returns the scan and the low-run length it was planned with.
+  auto greedy_step = [&](const std::vector<int>& pend) {
+    Scan best = best_scan(pend);
+    int L_used = Lbase;
     if (Lwide > Lbase) {
       Lmin = Lwide;
       mmax = T - Lmin;
-      Scan wide = best_scan(pending);
+      Scan wide = best_scan(pend);
       // scattered strided qubits (> 2 runs) cost 3-7x the HBM time at 128-B
       // chunks (measured): the wide candidate wins at >= 40 % of the gates;
       // window-shaped candidates keep the default unless it is >= 90 %
       const size_t need = high_runs(best) > 2 ? 4 : 9;
-      if (!wide.taken.empty() && wide.taken.size() * 10 >= best.taken.size() * need)
+      if (!wide.taken.empty() && wide.taken.size() * 10 >= best.taken.size() * need) {
         best = std::move(wide);
-      else {
-        Lmin = Lbase;
-        mmax = T - Lmin;
+        L_used = Lwide;
+      }
+      Lmin = Lbase;
+      mmax = T - Lmin;
+    }
+    return std::make_pair(std::move(best), L_used);
+  };
+  // Pass sequence: a small beam search over the greedy step and every
+  // window-shaped candidate (measured on the 1-D layered circuits: the
+  // most-gates-now choice can cost a pass later; beam width 4 x 4
+  // candidates).  Planning only: the kernels see the same kind of passes.
+  std::vector<std::pair<Scan, int>> seq;
+  {
+    std::vector<int> pend = pending;
+    while (!pend.empty()) {
+      auto st = greedy_step(pend);
+      pend = st.first.deferred;
+      seq.push_back(std::move(st));
+    }
+  }
+  // the beam's sequence replaces the greedy one only when it needs fewer
+  // passes (same count: the greedy plan, measured no slower)
+  const bool use_beam = !opt.no_window_search && mmax > 0 && n >= 20 && gates.size() >= 32 && seq.size() >= 3;
+  if (use_beam) {
+    struct Node {
+      std::vector<int> pend;
+      std::vector<std::pair<Scan, int>> path;
+      double cost = 0.0;
+    };
+    std::vector<Node> beam(1);
+    beam[0].pend = pending;
+    constexpr int kWidth = 4, kCand = 4;
+    while (true) {
+      const Node* done = nullptr;
+      for (const Node& nd : beam)
+        if (nd.pend.empty() && (!done || nd.cost < done->cost)) done = &nd;
+      if (done) {
+        if (done->path.size() < seq.size()) seq = done->path;
+        break;
+      }
+      if (beam[0].path.size() + 1 >= seq.size()) break;  // cannot beat the greedy count
+      std::vector<Node> next;
+      for (const Node& nd : beam) {
+        std::vector<std::pair<Scan, int>> cand;
+        cand.push_back(greedy_step(nd.pend));
+        std::vector<char> allowed(n, 0);
+        for (int a = Lbase; a + mmax <= n; ++a) {
+          std::fill(allowed.begin(), allowed.end(), 0);
+          for (int q = a; q < a + mmax; ++q) allowed[q] = 1;
+          Scan sc = scan(nd.pend, &allowed);
+          if (!sc.taken.empty()) cand.push_back(std::make_pair(std::move(sc), Lbase));
+        }
+        std::stable_sort(cand.begin() + 1, cand.end(), [](const auto& x, const auto& y) {
+          return x.first.taken.size() > y.first.taken.size();
+        });
+        int used = 0;
+        for (auto& c : cand) {
+          if (c.first.taken.empty() || used++ >= kCand) continue;
+          Node ch;
+          ch.pend = c.first.deferred;
+          ch.cost = nd.cost + c.first.cost;
+          ch.path = nd.path;
+          ch.path.push_back(c);
+          next.push_back(std::move(ch));
+        }
+      }
+      // fewest gates left first; duplicates (same remaining set) collapse
+      std::stable_sort(next.begin(), next.end(), [](const Node& x, const Node& y) {
+        return x.pend.size() != y.pend.size() ? x.pend.size() < y.pend.size() : x.cost < y.cost;
+      });
+      beam.clear();
+      for (Node& ch : next) {
+        bool dup = false;
+        for (const Node& b : beam) dup = dup || b.pend == ch.pend;
+        if (!dup) beam.push_back(std::move(ch));
+        if (int(beam.size()) == kWidth) break;
+      }
+      if (beam.empty()) {
+        err = "internal planner error: empty beam";
+        return false;
       }
     }
-    const bool ok = emit(best);
+  }
+  for (auto& st : seq) {
+    Lmin = st.second;
+    mmax = T - Lmin;
+    const bool ok = emit(st.first);
     Lmin = Lbase;
     mmax = T - Lmin;
     if (!ok) return false;
-    pending.swap(best.deferred);
   }
+  pending.clear();
 
   // Tail merge: the greedy scan can leave a last pass with a handful of gates
   // (QFT-30 c128 and layered-33 c128 ended with a one-gate pass -- a full HBM
