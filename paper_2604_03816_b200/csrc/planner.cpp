@@ -319,44 +319,18 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
     }
     return dense;
   };
-  while (!pending.empty()) {
-    std::vector<char> block_all(p.T, 0), block_dense(p.T, 0);
+  // One phase from `pend` with register set `fixed` (-1: first fit): the
+  // register bits, the ops it absorbs, the ops left.
+  struct PhaseStep {
     std::vector<int> R, took, rest;
-    // Register set: the RB tile bits that absorb the most dense ops (exhaustive
-    // over the bits the pending dense ops touch; fewer phases = fewer
-    // transposes, and a tensor-core phase costs the same whatever it holds).
-    // First-fit order decides only when fewer than RB bits are in play.
-    int cand = 0;
-    for (int i : pending)
-      if (p.ops[i].kind != OP_DIAG)
-        for (int j = 0; j < p.ops[i].k; ++j) cand |= 1 << p.ops[i].tgt[j];
-    int fixed = -1;
-    if (__builtin_popcount(cand) > RB && __builtin_popcount(cand) <= 16) {
-      std::vector<int> cb;
+  };
+  auto phase_with = [&](const std::vector<int>& pend, int fixed) {
+    PhaseStep ps;
+    std::vector<char> block_all(p.T, 0), block_dense(p.T, 0);
+    if (fixed >= 0)
       for (int b = 0; b < p.T; ++b)
-        if ((cand >> b) & 1) cb.push_back(b);
-      const int nb = int(cb.size());
-      int best = -1;
-      std::vector<int> sel(RB);
-      for (int i = 0; i < RB; ++i) sel[i] = i;
-      while (true) {  // all RB-subsets of cb, lexicographic
-        int mask = 0;
-        for (int i = 0; i < RB; ++i) mask |= 1 << cb[sel[i]];
-        const int got = absorbed(pending, mask);
-        if (got > best) {
-          best = got;
-          fixed = mask;
-        }
-        int i = RB - 1;
-        while (i >= 0 && sel[i] == nb - RB + i) --i;
-        if (i < 0) break;
-        ++sel[i];
-        for (int j = i + 1; j < RB; ++j) sel[j] = sel[j - 1] + 1;
-      }
-      for (int b = 0; b < p.T; ++b)
-        if ((fixed >> b) & 1) R.push_back(b);
-    }
-    for (int i : pending) {
+        if ((fixed >> b) & 1) ps.R.push_back(b);
+    for (int i : pend) {
       const KernelOp& op = p.ops[i];
       bool blocked = false;
       for (int j = 0; j < op.k && !blocked; ++j)
@@ -370,27 +344,122 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
           take = true;
           for (int j = 0; j < op.k; ++j) take = take && ((fixed >> op.tgt[j]) & 1);
         } else {
-          std::vector<int> u = R;
+          std::vector<int> u = ps.R;
           for (int j = 0; j < op.k; ++j)
             if (std::find(u.begin(), u.end(), op.tgt[j]) == u.end()) u.push_back(op.tgt[j]);
           if (int(u.size()) <= RB) {
-            R.swap(u);
+            ps.R.swap(u);
             take = true;
           }
         }
       }
       if (take) {
-        took.push_back(i);
+        ps.took.push_back(i);
       } else {
-        rest.push_back(i);
+        ps.rest.push_back(i);
         for (int j = 0; j < op.k; ++j)
           if (op.tgt[j] < p.T) (op.kind == OP_DIAG ? block_dense : block_all)[op.tgt[j]] = 1;
       }
     }
-    sets.push_back(R);
-    members.push_back(took);
-    pending.swap(rest);
+    return ps;
+  };
+  // Candidate register sets for a phase: every RB-subset of the bits the
+  // pending dense ops touch, ranked by the dense ops they absorb (fewer phases
+  // = fewer transposes / GEMMs); first fit when <= RB bits are in play.
+  auto candidates = [&](const std::vector<int>& pend, int keep) {
+    std::vector<std::pair<int, int>> got;  // (absorbed, mask)
+    int cand = 0;
+    for (int i : pend)
+      if (p.ops[i].kind != OP_DIAG)
+        for (int j = 0; j < p.ops[i].k; ++j) cand |= 1 << p.ops[i].tgt[j];
+    if (__builtin_popcount(cand) > RB && __builtin_popcount(cand) <= 16) {
+      std::vector<int> cb;
+      for (int b = 0; b < p.T; ++b)
+        if ((cand >> b) & 1) cb.push_back(b);
+      const int nb = int(cb.size());
+      std::vector<int> sel(RB);
+      for (int i = 0; i < RB; ++i) sel[i] = i;
+      while (true) {  // all RB-subsets of cb, lexicographic
+        int mask = 0;
+        for (int i = 0; i < RB; ++i) mask |= 1 << cb[sel[i]];
+        got.push_back({absorbed(pend, mask), mask});
+        int i = RB - 1;
+        while (i >= 0 && sel[i] == nb - RB + i) --i;
+        if (i < 0) break;
+        ++sel[i];
+        for (int j = i + 1; j < RB; ++j) sel[j] = sel[j - 1] + 1;
+      }
+      // most absorbed first; lexicographic order breaks ties (the greedy choice)
+      std::stable_sort(got.begin(), got.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      if (int(got.size()) > keep) got.resize(keep);
+    } else {
+      got.push_back({0, -1});
+    }
+    return got;
+  };
+  // greedy sequence
+  {
+    std::vector<int> pend = pending;
+    while (!pend.empty()) {
+      PhaseStep ps = phase_with(pend, candidates(pend, 1)[0].second);
+      sets.push_back(ps.R);
+      members.push_back(ps.took);
+      pend.swap(ps.rest);
+    }
   }
+  // beam over register-set choices (width 4, 4 candidates per phase), kept
+  // when it needs fewer phases -- each phase is a shared-memory transpose
+  // (c128) or a GEMM (c64); ~1.5-2 ms per phase at 30 q c128 (measured)
+  if (sets.size() >= 3) {
+    struct Node {
+      std::vector<int> pend;
+      std::vector<std::vector<int>> sets, members;
+    };
+    std::vector<Node> beam(1);
+    beam[0].pend = pending;
+    while (!beam.empty() && beam[0].sets.size() + 1 < sets.size()) {
+      std::vector<Node> next;
+      for (const Node& nd : beam)
+        for (const auto& c : candidates(nd.pend, 4)) {
+          PhaseStep ps = phase_with(nd.pend, c.second);
+          if (ps.took.empty()) continue;
+          Node ch;
+          ch.sets = nd.sets;
+          ch.members = nd.members;
+          ch.sets.push_back(ps.R);
+          ch.members.push_back(ps.took);
+          ch.pend.swap(ps.rest);
+          next.push_back(std::move(ch));
+        }
+      auto dense_left = [&](const Node& nd) {
+        int d = 0;
+        for (int i : nd.pend) d += p.ops[i].kind != OP_DIAG;
+        return d;
+      };
+      std::stable_sort(next.begin(), next.end(), [&](const Node& x, const Node& y) {
+        const int dx = dense_left(x), dy = dense_left(y);
+        return dx != dy ? dx < dy : x.pend.size() < y.pend.size();
+      });
+      beam.clear();
+      for (Node& ch : next) {
+        bool dup = false;
+        for (const Node& b : beam) dup = dup || b.pend == ch.pend;
+        if (!dup) beam.push_back(std::move(ch));
+        if (beam.size() == 4) break;
+      }
+      const Node* done = nullptr;
+      for (const Node& nd : beam)
+        if (nd.pend.empty()) done = &nd;
+      if (done) {
+        if (done->sets.size() < sets.size()) {
+          sets = done->sets;
+          members = done->members;
+        }
+        break;
+      }
+    }
+  }
+  pending.clear();
   if (int(sets.size()) > kMaxPhases) return false;
   // reorder ops into phase order
   std::vector<KernelOp> ordered;

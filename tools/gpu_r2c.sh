@@ -1,7 +1,10 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
-timeout 900 python -m pytest tests/test_gpu_parity_scale.py -m gpu -x -q --timeout 600 -k "not full_size_vs_oracle and not prefix" > gpurun_out/pytest_scale.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_scale.txt
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --pass-times > gpurun_out/bench_gemm.txt 2> gpurun_out/bench_gemm_passes.txt
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --streams 3 > gpurun_out/bench_gemm_s3.txt 2>&1
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --tensor-cores 2 > gpurun_out/bench_old.txt 2>&1
-tail -2 gpurun_out/pytest_gpu.txt gpurun_out/pytest_scale.txt
+: > gpurun_out/phbeam.txt
+for k in 1 2; do
+for cfg in "--config layered-30 --precision double" "--config qft30" ""; do
+  r=$(timeout 300 python bench.py --no-cpu-baseline --no-configs --steps 5 --warmup 2 $cfg 2>/dev/null | tail -1 | grep -o '"ms_per_step": [0-9.]*')
+  echo "$cfg $r" >> gpurun_out/phbeam.txt
+done
+done
+timeout 600 python bench.py --config layered33 --steps 2 --warmup 1 --no-cpu-baseline --no-configs > gpurun_out/bench_l33c.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_scale.py -m gpu -x -q --timeout 900 -k "not 32q" > gpurun_out/pytest_phbeam.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_phbeam.txt
