@@ -50,7 +50,7 @@ class PassInfo(C.Structure):
 
 
 KERNELS = ("tile", "reg", "reg_tc", "gemm")
-KINDS = ("dense", "diag", "perm")  # OpKind; "perm" = CNOT, targets (control, target)
+KINDS = ("dense", "diag", "perm", "ctrl")  # OpKind; "perm" = CNOT (control, target); "ctrl" = U0/U1 by a thread bit
 
 
 class NativeError(RuntimeError):
@@ -197,6 +197,8 @@ class NativePlan:
                "coeffs": co[:2 * n].view(np.complex128).copy()}
         if kind.value == 2:  # CNOT: control / target register bits
             out["ctrl"], out["tgt"] = int(src[0]), int(src[1])
+        if kind.value == 3:  # controlled op: target register mask, control thread bit
+            out["ctrl_thread_bit"] = int(src[0])
         if kind.value == 1:
             out["thread_bits"] = [int(x) for x in src[:mask.value]]
             out["rmap"] = src[8:16].view(np.uint8).copy()

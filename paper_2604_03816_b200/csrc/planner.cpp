@@ -278,7 +278,7 @@ void set_layout_flags(RegPhase& rp, int RB, int prec, bool first, bool last) {
 // are already scheduled and whose bits fit the phase's RB register bits
 // (diagonal ops fit any phase).  Ops are reordered into phase order.
 // Returns false when the pass must use the shared-memory kernel instead.
-bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
+bool build_phases(Pass& p, int RB, int prec, int TB = 8, bool allow_ctrl = false) {
   // instantiated register kernels: c64 RB 3..5, c128 RB 3..4 (8 thread bits);
   // the tensor-core kernel: c64 RB 5 with 7 thread bits
   if (TB == 8 && (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4))) return false;
@@ -301,20 +301,54 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   std::vector<int> pending(p.ops.size());
   for (size_t i = 0; i < p.ops.size(); ++i) pending[i] = int(i);
   std::vector<std::vector<int>> sets, members;
+  // Controlled 2q ops (block-diagonal in one qubit, exact zeros): only the
+  // target must be a register bit -- the control selects U0 / U1 per thread
+  // (OP_CTRL) -- and the control orders like a diagonal touch (a controlled-U
+  // commutes with diagonals on its control).  ctl[i] = local index of the
+  // control in tgt, or -1.
+  std::vector<int> ctl(p.ops.size(), -1);
+  if (allow_ctrl)
+    for (size_t i = 0; i < p.ops.size(); ++i) {
+      const KernelOp& op = p.ops[i];
+      if (op.kind != OP_DENSE || op.k != 2 || op.coeff.size() != 16) continue;
+      for (int b = 0; b < 2 && ctl[i] < 0; ++b) {
+        bool bd = true;
+        for (int r = 0; r < 4 && bd; ++r)
+          for (int c = 0; c < 4 && bd; ++c)
+            if (((r >> b) & 1) != ((c >> b) & 1)) bd = op.coeff[size_t(r) * 4 + c] == cd();
+        if (bd && op.tgt[b] < p.T && op.tgt[1 - b] < p.T) ctl[i] = b;
+      }
+    }
+  // bits an op needs in the register set / bits it touches like a dense op /
+  // bits it touches like a diagonal (for the ordering blocks)
+  auto need_bits = [&](int i) {
+    const KernelOp& op = p.ops[i];
+    int b = 0;
+    if (op.kind == OP_DIAG) return b;
+    for (int j = 0; j < op.k; ++j)
+      if (op.tgt[j] < p.T && j != ctl[i]) b |= 1 << op.tgt[j];
+    return b;
+  };
+  auto diagish_bits = [&](int i) {
+    const KernelOp& op = p.ops[i];
+    int b = 0;
+    for (int j = 0; j < op.k; ++j)
+      if (op.tgt[j] < p.T && (op.kind == OP_DIAG || j == ctl[i])) b |= 1 << op.tgt[j];
+    return b;
+  };
   // dense ops a phase with register set `mask` (tile bits) would absorb
   auto absorbed = [&](const std::vector<int>& pend, int mask) {
     int dense = 0, all_block = 0, dense_block = 0;
     for (int i : pend) {
       const KernelOp& op = p.ops[i];
-      int bits = 0;
-      for (int j = 0; j < op.k; ++j)
-        if (op.tgt[j] < p.T) bits |= 1 << op.tgt[j];
-      const bool blocked = (bits & all_block) || (op.kind != OP_DIAG && (bits & dense_block));
-      const bool take = !blocked && (op.kind == OP_DIAG || (bits & ~mask) == 0);
+      const int nb = need_bits(i), db = diagish_bits(i);
+      const bool blocked = ((nb | db) & all_block) || (nb & dense_block);
+      const bool take = !blocked && (op.kind == OP_DIAG || (nb & ~mask) == 0);
       if (take) {
         dense += op.kind != OP_DIAG;
       } else {
-        (op.kind == OP_DIAG ? dense_block : all_block) |= bits;
+        all_block |= nb;
+        dense_block |= db;
       }
     }
     return dense;
@@ -332,21 +366,20 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
         if ((fixed >> b) & 1) ps.R.push_back(b);
     for (int i : pend) {
       const KernelOp& op = p.ops[i];
+      const int nb = need_bits(i), db = diagish_bits(i);
       bool blocked = false;
-      for (int j = 0; j < op.k && !blocked; ++j)
-        blocked = op.tgt[j] < p.T &&
-                  (block_all[op.tgt[j]] || (op.kind != OP_DIAG && block_dense[op.tgt[j]]));
+      for (int b = 0; b < p.T && !blocked; ++b)
+        blocked = (((nb | db) >> b) & 1 && block_all[b]) || ((nb >> b) & 1 && block_dense[b]);
       bool take = false;
       if (!blocked) {
         if (op.kind == OP_DIAG) {
           take = true;
         } else if (fixed >= 0) {
-          take = true;
-          for (int j = 0; j < op.k; ++j) take = take && ((fixed >> op.tgt[j]) & 1);
+          take = (nb & ~fixed) == 0;
         } else {
           std::vector<int> u = ps.R;
-          for (int j = 0; j < op.k; ++j)
-            if (std::find(u.begin(), u.end(), op.tgt[j]) == u.end()) u.push_back(op.tgt[j]);
+          for (int b = 0; b < p.T; ++b)
+            if ((nb >> b) & 1 && std::find(u.begin(), u.end(), b) == u.end()) u.push_back(b);
           if (int(u.size()) <= RB) {
             ps.R.swap(u);
             take = true;
@@ -357,8 +390,10 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
         ps.took.push_back(i);
       } else {
         ps.rest.push_back(i);
-        for (int j = 0; j < op.k; ++j)
-          if (op.tgt[j] < p.T) (op.kind == OP_DIAG ? block_dense : block_all)[op.tgt[j]] = 1;
+        for (int b = 0; b < p.T; ++b) {
+          if ((nb >> b) & 1) block_all[b] = 1;
+          if ((db >> b) & 1) block_dense[b] = 1;
+        }
       }
     }
     return ps;
@@ -370,8 +405,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
     std::vector<std::pair<int, int>> got;  // (absorbed, mask)
     int cand = 0;
     for (int i : pend)
-      if (p.ops[i].kind != OP_DIAG)
-        for (int j = 0; j < p.ops[i].k; ++j) cand |= 1 << p.ops[i].tgt[j];
+      if (p.ops[i].kind != OP_DIAG) cand |= need_bits(i);
     if (__builtin_popcount(cand) > RB && __builtin_popcount(cand) <= 16) {
       std::vector<int> cb;
       for (int b = 0; b < p.T; ++b)
@@ -463,10 +497,14 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
   if (int(sets.size()) > kMaxPhases) return false;
   // reorder ops into phase order
   std::vector<KernelOp> ordered;
+  std::vector<int> ctl_o;
   std::vector<std::pair<int, int>> ranges;
   for (auto& mem : members) {
     const int b = int(ordered.size());
-    for (int i : mem) ordered.push_back(p.ops[i]);
+    for (int i : mem) {
+      ordered.push_back(p.ops[i]);
+      ctl_o.push_back(ctl[i]);
+    }
     ranges.emplace_back(b, int(ordered.size()));
   }
   p.ops.swap(ordered);
@@ -555,6 +593,21 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8) {
           for (int j = 0; j < kx; ++j) old |= ((int(nidx) >> (kr + kt + j)) & 1) << extb[j].second;
           ro.coeff[nidx] = op.coeff[old];
         }
+      } else if (op.kind == OP_DENSE && ctl_o[i] >= 0 && reg_of(op.tgt[ctl_o[i]]) < 0) {
+        // controlled op with its control on a thread bit: U0 / U1 on the target
+        const int cb = ctl_o[i], tb = 1 - cb;
+        const int rt = reg_of(op.tgt[tb]);
+        if (rt < 0) return false;  // cannot happen by construction
+        ro.kind = OP_CTRL;
+        ro.k = 1;
+        ro.mask = 1 << rt;
+        ro.src[0] = thread_bit_of(op.tgt[cb]);
+        ro.coeff.assign(8, cd());
+        for (int v = 0; v < 2; ++v)
+          for (int x = 0; x < 2; ++x)
+            for (int y = 0; y < 2; ++y)
+              ro.coeff[size_t(v) * 4 + x * 2 + y] =
+                  op.coeff[size_t((v << cb) | (x << tb)) * 4 + ((v << cb) | (y << tb))];
       } else if (op.kind == OP_PERM) {
         const int rc = reg_of(op.tgt[0]), rt = reg_of(op.tgt[1]);
         if (rc < 0 || rt < 0) return false;
@@ -1715,7 +1768,7 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
       // pass 93 % of HBM vs 80 % with four)
       p.streams = opt.streams == 2 ? 2 : opt.streams == 3 ? 3 : opt.streams == 4 ? 4 : (p.mma_phases ? 4 : 3);
     } else if (prec == SVB_C128 && opt.streams != 1 && (opt.reg_bits == 0 || opt.reg_bits == 4) && p.T == 11 &&
-               build_phases(p, 4, prec, 7)) {
+               build_phases(p, 4, prec, 7, !std::getenv("SVB_NO_CTRL"))) {
       // c128 default: tile streams of 11-qubit tiles, 16 amplitudes x 128
       // threads each (measured layered-30 395 ms with two vs 422 ms for one
       // stream of 12-qubit tiles: one group's transposes overlap another's
@@ -1726,7 +1779,7 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
     } else {
       int RB = opt.reg_bits > 0 ? opt.reg_bits : default_reg_bits(prec);
       if (p.T < RB + 8) RB = p.T - 8;  // small states: narrower register tile
-      if (!opt.no_reg_phases && !build_phases(p, RB, prec)) {
+      if (!opt.no_reg_phases && !build_phases(p, RB, prec, 8, prec == SVB_C128 && !std::getenv("SVB_NO_CTRL"))) {
         p.phases.clear();
         p.reg_ops.clear();
         p.reg_bits = 0;

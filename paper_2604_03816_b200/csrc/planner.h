@@ -60,7 +60,7 @@ struct RegOp {
   int k = 0;
   int stype = 0;           // dense 1q: DenseStructure
   int mask = 0;            // dense: register-bit mask; diagonal: kt (# thread-sourced bits)
-  int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j
+  int src[kMaxK] = {0};    // diagonal: thread bit of table bit kr + j; OP_CTRL: src[0] = control thread bit
   unsigned char rmap[32] = {0};  // diagonal: register part of the table index per rho
   int rmask = 0;                  // diagonal: register indices the table reads (its kr bits)
   int kx = 0;                     // diagonal: top kx table bits are shard qubits outside the tile

@@ -201,6 +201,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
           }
         }
       }
+      if (ro.kind == OP_CTRL) d.srt[0] = ro.src[0];  // control thread bit
       if (ro.kind == OP_DIAG) {
         std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];

@@ -26,7 +26,11 @@ constexpr int kThreads = kComputeThreads + 32;   // + one TMA producer warp
 // OP_PERM: a CNOT on tile bits (tgt[0] control, tgt[1] target): pairs of
 // amplitudes swapped, no arithmetic (the opt-in c128 factorisation of fused
 // gates; executed by the shared-memory kernel)
-enum OpKind : int { OP_DENSE = 0, OP_DIAG = 1, OP_PERM = 2 };
+enum OpKind : int { OP_DENSE = 0, OP_DIAG = 1, OP_PERM = 2, OP_CTRL = 3 };
+// OP_CTRL (register phases only): a 2-qubit gate that is block-diagonal in one
+// qubit, applied as U0 / U1 on the target register bit (pad = its mask),
+// selected by the control, which is a THREAD bit (srt[0]) -- the control
+// need not be a register bit of the phase.  coeff: U0 then U1, 2x2 each.
 // structure of a 1-qubit dense op's columns (planner bookkeeping of the
 // factorisation): ST_GENERAL, or each column purely real / purely imaginary
 enum DenseStructure : int { ST_GENERAL = 0, ST_RR = 1, ST_RI = 2, ST_IR = 3, ST_II = 4 };

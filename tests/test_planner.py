@@ -239,6 +239,18 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                             if rho & cm and not rho & tm:
                                 v[:, [rho, rho | tm]] = v[:, [rho | tm, rho]]
                         continue
+                    if op["kind"] == "ctrl":  # U0 / U1 on one register bit, chosen by a thread bit
+                        mask = op["mask"]
+                        sel = (tid >> op["ctrl_thread_bit"]) & 1
+                        Us = op["coeffs"].reshape(2, 2, 2).astype(v.dtype)
+                        rest = (nr - 1) & ~mask
+                        for g in range(1 << (rb - 1)):
+                            b0 = _deposit(g, rest, rb)
+                            c0, c1 = b0, b0 | mask
+                            a0, a1 = v[:, c0].copy(), v[:, c1].copy()
+                            v[:, c0] = Us[sel, 0, 0] * a0 + Us[sel, 0, 1] * a1
+                            v[:, c1] = Us[sel, 1, 0] * a0 + Us[sel, 1, 1] * a1
+                        continue
                     if op["kind"] == "dense":
                         k, mask = op["k"], op["mask"]
                         d = 1 << k
@@ -486,3 +498,18 @@ def test_gate_merge_of_unfused_runs():
     p2 = CircuitPlan(4, Precision.DOUBLE, g, plan_options(tensor_cores=-1, tile_bits=4, min_low_bits=1))
     assert np.abs(emulate(p2, 4, "double") - orc.run_circuit(c2, "double")).max() <= 1e-12
     assert sum(i["num_kernel_ops"] for i in p2.passes()) < len(g)
+
+
+def test_controlled_ops_on_thread_bits():
+    """Block-diagonal (controlled-U) 2q gates whose control is not a register
+    bit of the phase run as OP_CTRL (U0 / U1 selected by a thread bit): the
+    c128 layered and QFT plans use them, and the register-phase emulation with
+    them reproduces the oracle."""
+    for c in (fuse(gen.layered_circuit(13, layers=5, seed=3), 2)[0], fuse(gen.qft_circuit(12), 2)[0]):
+        plan = CircuitPlan(c.num_qubits, Precision.DOUBLE, c.gates)
+        infos = plan.passes()
+        kinds = [plan.native.phase_op(p, k)["kind"] for p in range(plan.num_passes)
+                 for k in range(infos[p]["num_kernel_ops"])]
+        assert "ctrl" in kinds
+        got = emulate_reg(plan, c.num_qubits, "double")
+        assert np.abs(got - orc.run_circuit(c, "double")).max() <= 1e-12

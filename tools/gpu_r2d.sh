@@ -1,5 +1,10 @@
 mkdir -p gpurun_out
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gemm_pass" -s 1 -c 3 \
-  -o gpurun_out/prof_gemm python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/prof_gemm.log 2>&1
-python tools/ncu_summary.py gpurun_out/prof_gemm.ncu-rep "gemm passes 1-3 layered-28" > gpurun_out/prof_gemm.txt 2>&1
-python tools/ncu_opstall.py gpurun_out/prof_gemm.ncu-rep > gpurun_out/prof_gemm_ops.txt 2>&1
+: > gpurun_out/ctrl.txt
+for k in 1 2; do
+for cfg in "--config layered-30 --precision double" "--config qft30"; do
+  r=$(timeout 300 python bench.py --no-cpu-baseline --no-configs --steps 5 --warmup 2 $cfg 2>/dev/null | tail -1 | grep -o '"ms_per_step": [0-9.]*')
+  echo "$cfg $r" >> gpurun_out/ctrl.txt
+done
+done
+timeout 600 python bench.py --config layered33 --steps 2 --warmup 1 --no-cpu-baseline --no-configs > gpurun_out/bench_l33d.txt 2>&1
+timeout 1500 python -m pytest tests/ -m gpu -x -q --timeout 900 > gpurun_out/pytest_ctrl.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_ctrl.txt

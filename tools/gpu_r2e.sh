@@ -1,7 +1,13 @@
 mkdir -p gpurun_out
-for s in 4 3 2; do
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --streams $s --pass-times > gpurun_out/bench_gemm_s$s.txt 2> gpurun_out/bench_gemm_s${s}_passes.txt
+: > gpurun_out/ctrl2.txt
+for k in 1 2; do
+for e in 0 1; do
+for cfg in "--config layered-30 --precision double" "--config qft30"; do
+  if [ $e = 1 ]; then export SVB_NO_CTRL=1; else unset SVB_NO_CTRL; fi
+  r=$(timeout 300 python bench.py --no-cpu-baseline --no-configs --steps 5 --warmup 2 $cfg 2>/dev/null | tail -1 | grep -o '"ms_per_step": [0-9.]*')
+  echo "noctrl=$e $cfg $r" >> gpurun_out/ctrl2.txt
 done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_gemm_pass" -s 1 -c 3 \
-  -o gpurun_out/prof_gemm python bench.py --steps 1 --warmup 0 --no-cpu-baseline --streams 3 > gpurun_out/prof_gemm.log 2>&1
-python tools/ncu_summary.py gpurun_out/prof_gemm.ncu-rep "gemm passes 1-3 layered-28 streams 3" > gpurun_out/prof_gemm.txt 2>&1
+done
+done
+unset SVB_NO_CTRL
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q --timeout 900 > gpurun_out/pytest_ctrl2.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_ctrl2.txt
