@@ -532,10 +532,37 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8, bool allow_ctrl = false
     rp.op_begin = ranges[ph].first;
     rp.op_end = ranges[ph].second;
     // register-FMA layout: register-index bit i <-> R[i], thread bits <-> the
-    // other tile bits ascending
+    // other tile bits ascending -- except that the first low_conflict lanes
+    // take tile bits of distinct residues mod low_conflict when the ascending
+    // order would not: the shared-memory swizzle XORs tile bits q into bank
+    // bit q mod low_conflict, so lanes whose tile bits share a residue hit the
+    // same banks (an 8-way conflict for lane bits {0, 3, 6} in c128, measured
+    // 19 % extra wavefronts once controlled ops freed the low bits)
     for (int i = 0; i < RB; ++i) rp.map[i] = R[i];
-    for (int q = 0, j = 0; q < p.T; ++q)
-      if (std::find(R.begin(), R.end(), q) == R.end()) rp.map[RB + j++] = q;
+    {
+      std::vector<int> th;
+      for (int q = 0; q < p.T; ++q)
+        if (std::find(R.begin(), R.end(), q) == R.end()) th.push_back(q);
+      std::vector<int> lanes, rest;
+      int seen = 0;
+      for (int q : th) {
+        const int r = q % low_conflict;
+        if (int(lanes.size()) < low_conflict && !((seen >> r) & 1)) {
+          lanes.push_back(q);
+          seen |= 1 << r;
+        } else {
+          rest.push_back(q);
+        }
+      }
+      // (c128 only: the c64 tensor-core phases need the ascending order)
+      if (int(lanes.size()) < low_conflict || prec != SVB_C128) {  // plain ascending order
+        lanes.clear();
+        rest = th;
+      }
+      int j = 0;
+      for (int q : lanes) rp.map[RB + j++] = q;
+      for (int q : rest) rp.map[RB + j++] = q;
+    }
     set_layout_flags(rp, RB, prec, ph == 0, ph + 1 == sets.size());
     auto reg_of = [&](int t) {
       for (int i = 0; i < RB; ++i)
@@ -543,10 +570,9 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8, bool allow_ctrl = false
       return -1;
     };
     auto thread_bit_of = [&](int t) {
-      int k = 0;
-      for (int q = 0; q < t; ++q)
-        if (std::find(R.begin(), R.end(), q) == R.end()) ++k;
-      return k;
+      for (int j = 0; j < p.T - RB; ++j)
+        if (rp.map[RB + j] == t) return j;
+      return -1;
     };
     for (int i = rp.op_begin; i < rp.op_end; ++i) {
       const KernelOp& op = p.ops[i];
