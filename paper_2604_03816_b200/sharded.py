@@ -329,30 +329,47 @@ class ShardedEngine:
         """Every rank's shard mapped into this process (CUDA IPC).  Handles
         are gathered at every exchange (a re-allocated shard gets a new
         handle even at a recycled address); mappings are cached per handle."""
+        import torch
+
         from . import _native
-        mine = _native.ipc_export(t.data_ptr())
+        try:
+            mine = _native.ipc_export(t.data_ptr())
+        except Exception:  # e.g. a driver without IPC: every rank falls back together
+            mine = None
         allh = [None] * self.world
         self.dist.all_gather_object(allh, mine, group=self.group)
-        ptrs = {}
-        for r, (h, off) in enumerate(allh):
+        ptrs, ok = {}, all(x is not None for x in allh)
+        for r, hx in enumerate(allh if ok else []):
+            h, off = hx
             if r == self.rank:
                 ptrs[r] = t.data_ptr()
                 continue
-            if h not in self._peers:
-                _ptr, base = _native.ipc_import(h, 0)
-                self._peers[h] = base
-                self._bases.append(base)
-            ptrs[r] = self._peers[h] + off
-        return ptrs
+            try:
+                if h not in self._peers:
+                    _ptr, base = _native.ipc_import(h, 0)
+                    self._peers[h] = base
+                    self._bases.append(base)
+                ptrs[r] = self._peers[h] + off
+            except Exception:
+                ok = False
+                break
+        # every rank must agree (a one-sided fallback would deadlock the swap)
+        dev = t.device if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        return ptrs if int(flag.item()) == 1 else None
 
-    def _exchange_p2p_step(self, t, step, blk: int, peers) -> None:
+    def _exchange_p2p_step(self, t, step, blk: int, peers) -> bool:
         """Block swaps as one kernel per rank over peer-mapped memory: the pair
         (our block w, peer's block own(rank)) is split in halves, the lower
-        rank swaps the first, the higher the second, both at once."""
+        rank swaps the first, the higher the second, both at once.  False when
+        some rank cannot map its peers (the caller falls back to NCCL)."""
         import torch
 
         from . import _native
         ptrs = self._peer_ptrs(t)
+        if ptrs is None:
+            return False
         esz = t.element_size()
         total = blk * esz
         half = (total // 2) // 16 * 16
@@ -368,6 +385,7 @@ class ShardedEngine:
                 _native.swap_blocks(a0 + lo, b0 + lo, hi - lo, stream)
         torch.cuda.synchronize(t.device)    # our half of every pair is swapped ...
         self.dist.barrier(group=self.group)  # ... and the peers' halves
+        return True
 
     # -------------------------------------------------------------- program
     def compile(self, circuit, precision=Precision.DOUBLE):
@@ -424,10 +442,11 @@ class ShardedEngine:
             return
         npeer = len(peers)
         if self._use_p2p(t) and (blk * t.element_size()) % 16 == 0:
-            self._exchange_p2p_step(t, step, blk, peers)
-            if hasattr(state, "touch"):
-                state.touch()
-            return
+            if self._exchange_p2p_step(t, step, blk, peers):
+                if hasattr(state, "touch"):
+                    state.touch()
+                return
+            self.p2p = False  # IPC unavailable on some rank: NCCL point-to-point from now on
         if t.is_cuda and dist.get_backend(self.group) == "gloo":
             # gloo moves host tensors only (used by the single-GPU multi-process
             # tests): stage each block through host memory
