@@ -197,7 +197,8 @@ class NativePlan:
                "coeffs": co[:2 * n].view(np.complex128).copy()}
         if kind.value == 2:  # CNOT: control / target register bits
             out["ctrl"], out["tgt"] = int(src[0]), int(src[1])
-        if kind.value == 3:  # controlled op: target register mask, control thread bit
+        if kind.value == 3:  # controlled op: target register mask; control thread bit, or
+            # (negative) the shard qubit -1 - src[0] outside the tile
             out["ctrl_thread_bit"] = int(src[0])
         if kind.value == 1:
             out["thread_bits"] = [int(x) for x in src[:mask.value]]
@@ -220,8 +221,11 @@ class NativePlan:
         n = check(lib().svb_plan_kernel_op(self._h, p, i, C.byref(kind), C.byref(k), _iptr(tg),
                                            _dptr(co), 4096))
         coeffs = co[:2 * n].view(np.complex128).copy()
-        return {"kind": KINDS[kind.value], "k": k.value,
-                "targets": [int(t) for t in tg[:k.value]], "coeffs": coeffs}
+        out = {"kind": KINDS[kind.value], "k": k.value,
+               "targets": [int(t) for t in tg[:k.value]], "coeffs": coeffs}
+        if kind.value == 3:  # controlled op: U0 / U1 on targets[0], control = shard qubit outside the tile
+            out["ctrl_qubit"] = int(tg[1])
+        return out
 
     def execute(self, amps_ptr: int, stream: int, first: int = 0, count: int | None = None):
         if count is None:

@@ -619,6 +619,15 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8, bool allow_ctrl = false
           for (int j = 0; j < kx; ++j) old |= ((int(nidx) >> (kr + kt + j)) & 1) << extb[j].second;
           ro.coeff[nidx] = op.coeff[old];
         }
+      } else if (op.kind == OP_DENSE && op.ctlq >= 0) {
+        // controlled op with its control outside the tile (chosen per tile)
+        const int rt = reg_of(op.tgt[0]);
+        if (rt < 0) return false;  // cannot happen by construction
+        ro.kind = OP_CTRL;
+        ro.k = 1;
+        ro.mask = 1 << rt;
+        ro.src[0] = -1 - op.ctlq;
+        ro.coeff = op.coeff;
       } else if (op.kind == OP_DENSE && ctl_o[i] >= 0 && reg_of(op.tgt[ctl_o[i]]) < 0) {
         // controlled op with its control on a thread bit: U0 / U1 on the target
         const int cb = ctl_o[i], tb = 1 - cb;
@@ -1452,7 +1461,7 @@ bool make_gates(int n, int n_ops, const int* op_k, const int* op_targets, const 
 }
 
 bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const svb_plan_options& opt_in,
-                       Plan& plan, std::string& err) {
+                       Plan& plan, std::string& err, bool ctlx = true) {
   if (n < 1 || n > 62) {
     err = "n_local must be in 1..62";
     return false;
@@ -1507,10 +1516,27 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
   plan.opt = opt;
   plan.passes.clear();
 
+  // c128: 2q gates that are block-diagonal in one qubit (controlled-U, exact
+  // zeros) need only their target in the tile -- the control may be a shard
+  // qubit outside it (U0 / U1 chosen per tile), and it orders like a diagonal
+  // touch.  gctl[i] = local index of that control, or -1.
+  std::vector<int> gctl(gates.size(), -1);
+  if (ctlx && prec == SVB_C128 && !std::getenv("SVB_NO_CTRLX"))
+    for (size_t i = 0; i < gates.size(); ++i) {
+      const Gate& g = gates[i];
+      if (g.diag || g.k != 2 || g.m.size() != 16) continue;
+      for (int b = 0; b < 2 && gctl[i] < 0; ++b) {
+        bool bd = true;
+        for (int r = 0; r < 4 && bd; ++r)
+          for (int c = 0; c < 4 && bd; ++c)
+            if (((r >> b) & 1) != ((c >> b) & 1)) bd = g.m[size_t(r) * 4 + c] == cd();
+        if (bd) gctl[i] = b;
+      }
+    }
   for (size_t i = 0; i < gates.size(); ++i) {
     int high_needed = 0;  // diagonal gates need no tile qubits (bits outside the tile are per-tile constants)
     if (!gates[i].diag)
-      for (int j = 0; j < gates[i].k; ++j) high_needed += gates[i].t[j] >= Lmin;
+      for (int j = 0; j < gates[i].k; ++j) high_needed += gates[i].t[j] >= Lmin && j != gctl[i];
     if (high_needed > mmax) {
       err = "gate " + std::to_string(i) + " needs more strided tile bits than the tile allows";
       return false;
@@ -1542,15 +1568,16 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
     const bool merging = !opt.no_diag_merge;
     for (int gi : pend) {
       const Gate& g = gates[gi];
+      const int gc = gctl[gi];  // a control that may stay outside the tile
       bool blocked = false;
       for (int j = 0; j < g.k && !blocked; ++j)
-        blocked = block_all[g.t[j]] || (!g.diag && block_dense[g.t[j]]);
+        blocked = block_all[g.t[j]] || (!g.diag && j != gc && block_dense[g.t[j]]);
       bool take = false;
       if (!blocked) {
         int extra = 0;
         bool outside = false;
         for (int j = 0; j < g.k; ++j)
-          if (!g.diag && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+          if (!g.diag && j != gc && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
             ++extra;
             outside |= allowed && !(*allowed)[g.t[j]];
           }
@@ -1593,7 +1620,7 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
                (r.taken.empty() || budget < 0 || r.cost + c <= budget);
         if (take) {
           for (int j = 0; j < g.k; ++j)
-            if (!g.diag && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
+            if (!g.diag && j != gc && g.t[j] >= Lmin && !r.in_high[g.t[j]]) {
               r.in_high[g.t[j]] = 1;
               ++n_high;
             }
@@ -1607,7 +1634,7 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
       }
       if (!take) {
         r.deferred.push_back(gi);
-        for (int j = 0; j < g.k; ++j) (g.diag ? block_dense : block_all)[g.t[j]] = 1;
+        for (int j = 0; j < g.k; ++j) ((g.diag || j == gc) ? block_dense : block_all)[g.t[j]] = 1;
       }
     }
     return r;
@@ -1680,6 +1707,22 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
     };
     auto lower_plain = [&](int gi) {
       const Gate& g = gates[gi];
+      if (!g.diag && gctl[gi] >= 0 && local(g.t[gctl[gi]]) < 0) {
+        // controlled op, control outside the tile: U0 / U1 on the target
+        const int cb = gctl[gi], tb = 1 - cb;
+        KernelOp op;
+        op.kind = OP_DENSE;
+        op.k = 1;
+        op.tgt[0] = local(g.t[tb]);
+        op.ctlq = g.t[cb];
+        op.coeff.assign(8, cd());
+        for (int v = 0; v < 2; ++v)
+          for (int x = 0; x < 2; ++x)
+            for (int y = 0; y < 2; ++y)
+              op.coeff[size_t(v) * 4 + x * 2 + y] = g.m[size_t((v << cb) | (x << tb)) * 4 + ((v << cb) | (y << tb))];
+        op.gates.push_back(gi);
+        return op;
+      }
       if (g.diag) {  // sorted table bits (shard bits outside the tile last)
         int tg[kMaxK];
         for (int j = 0; j < g.k; ++j) tg[j] = dloc(g.t[j]);
@@ -1716,6 +1759,15 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
           continue;
         }
         Factor2q fz;
+        const bool cx = gctl[gi] >= 0 && local(g.t[gctl[gi]]) < 0;  // control outside the tile
+        if (cx) {
+          // close an open diagonal run the gate touches on either qubit (the
+          // pass scan's op-count and pool model does the same)
+          int tt[2] = {local(g.t[1 - gctl[gi]]), dloc(g.t[gctl[gi]])};
+          if (!acc.empty() && acc.touches(tt, 2)) ops.push_back(acc.take());
+          ops.push_back(lower_plain(gi));
+          continue;
+        }
         if (factor && g.k == 2 && factor_2q(g.m, fz) && factored_cost(fz) < 16.0) {
           if (!acc.empty() && acc.touches(tg, g.k)) ops.push_back(acc.take());
           for (int side = 0; side < 2; ++side) {
@@ -2000,6 +2052,18 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
       for (auto& th : pool) th.join();
     }
   }
+  // outside-tile controls exist only in register-phase kernels: a pass that
+  // ended on another kernel re-plans the whole circuit without them
+  for (const Pass& ps : plan.passes)
+    for (const KernelOp& o : ps.ops)
+      if (o.ctlq >= 0 && (ps.phases.empty() || ps.gemm)) {
+        if (!ctlx) {
+          err = "internal planner error: outside control in a non-register pass";
+          return false;
+        }
+        plan.passes.clear();
+        return build_plan_merged(n, prec, gates, opt_in, plan, err, false);
+      }
   return true;
 }
 
@@ -2113,7 +2177,14 @@ bool build_plan(int n, int prec, const std::vector<Gate>& gates_in, const svb_pl
   std::vector<Gate> merged;
   if (!opt_in.no_gate_merge) merged = merge_gates(gates_in, n, orig);
   const std::vector<Gate>& gates = opt_in.no_gate_merge ? gates_in : merged;
-  if (!build_plan_merged(n, prec, gates, opt_in, plan, err)) return false;
+  if (!build_plan_merged(n, prec, gates, opt_in, plan, err)) {
+    // outside-tile controls change the pass partition; if that partition
+    // cannot be lowered, plan without them before giving up
+    std::string err2;
+    plan.passes.clear();
+    if (!build_plan_merged(n, prec, gates, opt_in, plan, err2, false)) return false;
+    err.clear();
+  }
   if (opt_in.no_gate_merge) return true;
   // input-gate indices everywhere (pass_gates, reports, tests)
   auto remap = [&](std::vector<int>& v) {

@@ -35,6 +35,9 @@ struct KernelOp {
                            // (always the top table bits, ascending)
   std::vector<cd> coeff;
   std::vector<int> gates;  // input gates folded into this op, program order
+  int ctlq = -1;           // c128 controlled op with its control OUTSIDE the tile:
+                           // the control's shard qubit; k = 1 (tgt[0] = target),
+                           // coeff = U0 then U1 (2x2 each), chosen per tile
 };
 
 // Register-phase encoding of a pass for k_reg_pass (see svb_regpass.cuh).

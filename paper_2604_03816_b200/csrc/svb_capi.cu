@@ -201,7 +201,10 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
           }
         }
       }
-      if (ro.kind == OP_CTRL) d.srt[0] = ro.src[0];  // control thread bit
+      if (ro.kind == OP_CTRL) {  // control thread bit, or (srt[0] = -1) shard qubit tgt[0] outside the tile
+        d.srt[0] = ro.src[0] >= 0 ? ro.src[0] : -1;
+        d.tgt[0] = ro.src[0] >= 0 ? 0 : -1 - ro.src[0];
+      }
       if (ro.kind == OP_DIAG) {
         std::memcpy(d.tgt, ro.rmap, sizeof(ro.rmap));
         for (int j = 0; j < ro.mask; ++j) d.srt[j] = ro.src[j];
@@ -847,9 +850,10 @@ int svb_plan_kernel_op(const svb_plan* plan, int pass, int i, int* kind, int* k,
   const Pass& p = plan->plan.passes[pass];
   if (i < 0 || i >= int(p.ops.size())) return fail(SVB_EINVAL, "op index out of range");
   const KernelOp& op = p.ops[i];
-  *kind = op.kind;
+  *kind = op.ctlq >= 0 ? OP_CTRL : op.kind;  // controlled op, control = shard qubit tile_targets[1]
   *k = op.k;
   for (int j = 0; j < op.k; ++j) tile_targets[j] = op.tgt[j];
+  if (op.ctlq >= 0) tile_targets[1] = op.ctlq;
   if (coeffs) {
     if (int(op.coeff.size()) > coeff_cap) return fail(SVB_EINVAL, "coefficient capacity too small");
     for (size_t e = 0; e < op.coeff.size(); ++e) {

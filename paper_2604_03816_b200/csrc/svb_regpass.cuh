@@ -208,8 +208,12 @@ __device__ __forceinline__ void reg_dense2(C (&v)[1 << RB], const C* __restrict_
 // OP_CTRL ops (U0 / U1 on one register bit by the control thread bit srt[0])
 // share the 1-qubit dense code: only the coefficient pointer differs.
 template <class C, int RB, bool HOIST = true, int SP = 0, bool D3 = true>
-__device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool, int gt = 0) {
-  const C* co = pool + op.coeff_off + (op.kind == OP_CTRL ? 4 * ((gt >> op.srt[0]) & 1) : 0);
+__device__ __forceinline__ void reg_dense_op(C (&v)[1 << RB], const OpDesc& op, const C* pool, int gt = 0,
+                                             long long origin = 0) {
+  const C* co = pool + op.coeff_off +
+                (op.kind == OP_CTRL
+                     ? 4 * (op.srt[0] >= 0 ? (gt >> op.srt[0]) & 1 : int((origin >> op.tgt[0]) & 1))
+                     : 0);
   switch (op.pad) {  // register-bit mask of the dense op
 #define SVB_CASE(m) \
   case m:           \
@@ -869,7 +873,8 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
           reg_diag<C, RB>(v, op, pool + op.coeff_off,
                           int(dthr[o * NTG + gt]) | (h.has_outside ? dout[xs * kMaxOps + o] : 0));
         else
-          reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4), SP, !(sizeof(C) == 16 && TB == 7)>(v, op, pool, gt);
+          reg_dense_op<C, RB, !(sizeof(C) == 16 && NGRP >= 4), SP, !(sizeof(C) == 16 && TB == 7)>(v, op, pool, gt,
+                                                                                                 origin);
       }
       if constexpr (sizeof(C) == 8 && RB == 5) {
         if (last && h.renorm) {

@@ -54,6 +54,10 @@ def emulate_tile_pass(amps: np.ndarray, nat, p: int, n: int) -> None:
                 if op["kind"] == "dense":
                     u = op["coeffs"].reshape(1 << op["k"], 1 << op["k"])
                     orc.apply_matrix(buf, T, op["targets"], u)
+                elif op["kind"] == "ctrl":  # U0 / U1 on a tile bit, control = shard qubit outside the tile
+                    sel = int(idx[0] >> op["ctrl_qubit"]) & 1
+                    u = op["coeffs"].reshape(2, 2, 2)[sel]
+                    orc.apply_matrix(buf, T, op["targets"], u)
                 elif op["kind"] == "perm":  # CNOT(control, target) on tile bits
                     c_, t_ = op["targets"]
                     e = np.arange(1 << T)
@@ -240,8 +244,9 @@ def emulate_reg(plan: CircuitPlan, n: int, precision: str) -> np.ndarray:
                                 v[:, [rho, rho | tm]] = v[:, [rho | tm, rho]]
                         continue
                     if op["kind"] == "ctrl":  # U0 / U1 on one register bit, chosen by a thread bit
-                        mask = op["mask"]
-                        sel = (tid >> op["ctrl_thread_bit"]) & 1
+                        mask = op["mask"]           # or by a shard qubit outside the tile
+                        ctb = op["ctrl_thread_bit"]
+                        sel = (tid >> ctb) & 1 if ctb >= 0 else np.full(nthreads, int(idx[0] >> (-1 - ctb)) & 1)
                         Us = op["coeffs"].reshape(2, 2, 2).astype(v.dtype)
                         rest = (nr - 1) & ~mask
                         for g in range(1 << (rb - 1)):
@@ -513,3 +518,26 @@ def test_controlled_ops_on_thread_bits():
         assert "ctrl" in kinds
         got = emulate_reg(plan, c.num_qubits, "double")
         assert np.abs(got - orc.run_circuit(c, "double")).max() <= 1e-12
+
+
+def test_controls_outside_the_tile():
+    """c128: a controlled 2q gate needs only its target in the tile; with the
+    control outside, the pass applies U0 / U1 per tile (kernel op "ctrl",
+    phase op with a negative control thread bit).  Both emulations (tile
+    kernel view and register phases) reproduce the oracle, and switching the
+    feature off (SVB_NO_CTRLX) costs passes on a layered circuit."""
+    import os
+    c = fuse(gen.layered_circuit(16, layers=8, seed=5), 2)[0]
+    plan = CircuitPlan(16, Precision.DOUBLE, c.gates)
+    infos = plan.passes()
+    kops = [plan.native.kernel_op(p, k) for p in range(plan.num_passes) for k in range(infos[p]["num_kernel_ops"])]
+    assert any(o["kind"] == "ctrl" for o in kops)
+    want = orc.run_circuit(c, "double")
+    assert np.abs(plan_order_state(plan, c, "double") - want).max() <= 1e-12
+    assert np.abs(emulate_reg(plan, 16, "double") - want).max() <= 1e-12
+    os.environ["SVB_NO_CTRLX"] = "1"
+    try:
+        plain = CircuitPlan(16, Precision.DOUBLE, c.gates)
+    finally:
+        del os.environ["SVB_NO_CTRLX"]
+    assert plan.num_passes <= plain.num_passes
