@@ -168,6 +168,42 @@ def plan_kernels(plan) -> str:
     return "+".join(sorted(names))
 
 
+def gate_flops_per_amp(fused):
+    """Algorithmic real flops per amplitude of a fused circuit: a row of a
+    gate with r non-zeros costs r complex multiplies and r-1 complex adds
+    (8r - 2 flops; 6 for a diagonal, 8*2^k - 2 for a dense k-qubit gate)."""
+    from paper_2604_03816_b200.circuit import effective_unitary as _eu
+    total = 0
+    for op in fused.gates:
+        u = _eu(op)
+        r = np.count_nonzero(u) / u.shape[0]
+        total += 8 * r - 2
+    return total
+
+
+def fma_peak_tflops(device, prec, sm_mhz):
+    """Vector FMA peak: SMs x FMA/clk/SM (FP32 128, FP64 64) x 2 x SM clock."""
+    import torch
+    fma_per_clk = 128 if prec == "single" else 64
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return sms * fma_per_clk * 2 * sm_mhz * 1e6 / 1e12
+
+
+def compute_roofline(fused, n, pass_ms, peak_tflops):
+    """FP64 (c128 configs) compute roofline: the gates' algorithmic flops
+    over the summed pass time vs the vector FMA peak. c128 passes of layered
+    circuits are bound here rather than by HBM."""
+    fa = gate_flops_per_amp(fused)
+    ach = fa * (1 << n) / (sum(pass_ms) / 1e3) / 1e12
+    return {"bound": "fp64-fma", "achieved": ach, "peak": peak_tflops, "unit": "TFLOP/s",
+            "frac": ach / peak_tflops, "flops_per_amp": fa,
+            "floor_ms": fa * (1 << n) / (peak_tflops * 1e12) * 1e3,
+            "note": "algorithmic flops of the fused gates (8 per complex MAC over each row's "
+                    "non-zeros) vs SMs x 64 DFMA/clk x 2 x max SM clock; the kernel merges runs of "
+                    "diagonal gates into one table multiply, so diagonal-heavy circuits (QFT) execute "
+                    "fewer flops than counted"}
+
+
 def tensor_flops(plan, n: int) -> float:
     """Tensor-core flops of one plan execution: each GEMM phase multiplies every
     amplitude's 64-real row by a 64 x 64 real block in three fp16 products
@@ -385,16 +421,9 @@ def run_b200(args):
     # gates (dense k-qubit: 8*2^k - 2 real flops per amplitude, diagonal: 6)
     # against the vector FMA peak, and the tensor-core flops the GEMM phases
     # issue against the measured dense fp16 peak
-    from paper_2604_03816_b200.circuit import effective_unitary as _eu
-    flops_amp = 0
-    for op in fused.gates:
-        u = _eu(op)
-        k = len(op.targets)
-        flops_amp += 6 if np.count_nonzero(u - np.diag(np.diag(u))) == 0 else 8 * (1 << k) - 2
+    flops_amp = gate_flops_per_amp(fused)
     sm_mhz = (m_clk or {}).get("sm_max_mhz") or 1965.0
-    fma_per_clk = 128 if prec == "single" else 64
-    dev_props = torch.cuda.get_device_properties(local)
-    peak_tflops = dev_props.multi_processor_count * fma_per_clk * 2 * sm_mhz * 1e6 / 1e12
+    peak_tflops = fma_peak_tflops(local, prec, sm_mhz)
     achieved_tflops = flops_amp * (1 << n) / (sum(pass_ms) / 1e3) / 1e12
     tc_flops = tensor_flops(plan, n)
     tpeak, tpeak_kind = measured_peak_tensor()
@@ -422,6 +451,8 @@ def run_b200(args):
                                           "unit": "GB/s", "frac": b2 / (apm / 1e3) / 1e9 / peak,
                                           "peak_kind": peak_kind, "avg_launch_ms": apm,
                                           "traffic": measured_traffic(name.split("_")[0], pr, circ.num_qubits)},
+                             "compute": compute_roofline(f2, circ.num_qubits, mm["pass_ms"],
+                                                         fma_peak_tflops(local, pr, sm_mhz)),
                              "norm_after": mm["norm"], "clocks": mm["clocks"]}
             eng_state = mm.pop("state")
             del eng_state, mm
