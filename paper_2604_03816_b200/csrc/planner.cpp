@@ -1508,7 +1508,7 @@ bool build_plan_merged(int n, int prec, const std::vector<Gate>& gates, const sv
   const double default_budget =
       opt.cost_budget == 0.0 ? default_cost_budget(prec) : opt.cost_budget;
   double budget = default_budget;  // the tail merge below lifts it
-  const size_t pool_cap = size_t(kCoeffBytes) / (prec == SVB_C64 ? 8 : 16);
+  const size_t pool_cap = prec == SVB_C64 ? size_t(kPoolBytesC64) / 8 : size_t(kPoolBytesC128) / 16;
   const CostModel cm(prec);
 
   plan.n = n;

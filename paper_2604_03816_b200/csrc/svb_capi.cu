@@ -114,8 +114,18 @@ int device_facts(DeviceFacts** out) {
 }
 
 template <class C>
-void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) {
+void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a, std::vector<C>& ext) {
   std::memset(&a.h, 0, sizeof(a.h));
+  ext.clear();
+  // pool elements past the parameter block go to `ext` (global memory at launch)
+  constexpr int kParam = kCoeffBytes / int(sizeof(C));
+  auto put = [&](int off, const cd& z) {
+    C c;
+    c.x = static_cast<decltype(c.x)>(z.real());
+    c.y = static_cast<decltype(c.x)>(z.imag());
+    if (off < kParam) a.coeff[off] = c;
+    else ext.push_back(c);
+  };
   a.h.T = p.T;
   a.h.L = p.L;
   a.h.m = p.m;
@@ -213,11 +223,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
         d.xmask = ro.xmask;
         if (ro.kx) a.h.has_outside = 1;
       }
-      for (const cd& z : ro.coeff) {
-        a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
-        a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
-        ++off;
-      }
+      for (const cd& z : ro.coeff) put(off++, z);
     }
     a.h.coeff_count = off;
     return;
@@ -238,11 +244,7 @@ void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a) 
       d.tgt[j] = d.srt[j] = ko.tgt[j];
     }
     std::sort(d.srt, d.srt + ko.k - d.kx);
-    for (const cd& z : ko.coeff) {
-      a.coeff[off].x = static_cast<decltype(a.coeff[0].x)>(z.real());
-      a.coeff[off].y = static_cast<decltype(a.coeff[0].x)>(z.imag());
-      ++off;
-    }
+    for (const cd& z : ko.coeff) put(off++, z);
   }
   a.h.coeff_count = off;
 }
@@ -260,6 +262,12 @@ struct svb_plan {
   std::vector<size_t> tc_offset;  // per pass, in floats
   float* tc_dev = nullptr;
   int tc_dev_id = -1;
+  // coefficient pool past the parameter block, per pass (c128 passes with
+  // large diagonal tables); packed host copy, uploaded with the GEMM matrices
+  std::vector<unsigned char> ext_host;
+  std::vector<size_t> ext_offset;  // per pass, bytes (SIZE_MAX: none)
+  unsigned char* ext_dev = nullptr;
+  int ext_dev_id = -1;
   // execute_range writes the launch-time fields (tensor map of the state, TMA
   // ring depth) into the cached parameter blocks: one launcher at a time
   std::mutex mu;
@@ -268,6 +276,7 @@ struct svb_plan {
 
   ~svb_plan() {
     if (tc_dev) cudaFree(tc_dev);
+    if (ext_dev) cudaFree(ext_dev);
     for (auto& kv : normacc) cudaFree(kv.second);
   }
 };
@@ -539,7 +548,29 @@ void pack_tc(svb_plan* p) {
   }
 }
 
+template <class C>
+void point_ext(svb_plan* p, std::vector<PassArgs<C>>& args) {
+  for (size_t i = 0; i < args.size(); ++i)
+    args[i].h.coeff_ext = p->ext_offset[i] == SIZE_MAX ? nullptr : p->ext_dev + p->ext_offset[i];
+}
+
+int upload_ext(svb_plan* p) {
+  if (p->ext_host.empty()) return SVB_OK;
+  int dev = 0;
+  SVB_CUDA(cudaGetDevice(&dev));
+  if (p->ext_dev && p->ext_dev_id == dev) return SVB_OK;
+  if (p->ext_dev) cudaFree(p->ext_dev);
+  p->ext_dev = nullptr;
+  SVB_CUDA(cudaMalloc(&p->ext_dev, p->ext_host.size()));
+  SVB_CUDA(cudaMemcpy(p->ext_dev, p->ext_host.data(), p->ext_host.size(), cudaMemcpyHostToDevice));
+  p->ext_dev_id = dev;
+  point_ext(p, p->args64);
+  point_ext(p, p->args128);
+  return SVB_OK;
+}
+
 int upload_tc(svb_plan* p) {
+  if (int rc = upload_ext(p)) return rc;
   if (p->tc_host.empty()) return SVB_OK;
   int dev = 0;
   SVB_CUDA(cudaGetDevice(&dev));
@@ -687,17 +718,29 @@ int svb_plan_create(int n_local, int prec, int n_ops, const int* op_k, const int
   pack_tc(p.get());
   const int np = int(p->plan.passes.size());
   const long long n_tiles = 1LL << (n_local - (np ? p->plan.passes[0].T : 0));
+  p->ext_offset.assign(np, SIZE_MAX);
+  auto keep_ext = [&](int i, const auto& ext) {
+    if (ext.empty()) return;
+    p->ext_offset[i] = p->ext_host.size();
+    const auto* b = reinterpret_cast<const unsigned char*>(ext.data());
+    p->ext_host.insert(p->ext_host.end(), b, b + ext.size() * sizeof(ext[0]));
+    while (p->ext_host.size() % 256) p->ext_host.push_back(0);
+  };
   if (prec == SVB_C64) {
     p->args64.resize(np);
+    std::vector<float2> ext;
     for (int i = 0; i < np; ++i) {
-      fill_args<float2>(p->plan.passes[i], p->stages, n_local, p->args64[i]);
+      fill_args<float2>(p->plan.passes[i], p->stages, n_local, p->args64[i], ext);
       p->args64[i].h.n_tiles = n_tiles;
+      keep_ext(i, ext);
     }
   } else {
     p->args128.resize(np);
+    std::vector<double2> ext;
     for (int i = 0; i < np; ++i) {
-      fill_args<double2>(p->plan.passes[i], p->stages, n_local, p->args128[i]);
+      fill_args<double2>(p->plan.passes[i], p->stages, n_local, p->args128[i], ext);
       p->args128[i].h.n_tiles = n_tiles;
+      keep_ext(i, ext);
     }
   }
   *out = p.release();

@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(NG * WPG * 32, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int e = tid; e < h.coeff_count; e += NG * NTG) pool[e] = args.coeff[e];
+  for (int e = tid; e < h.coeff_count; e += NG * NTG) pool[e] = pool_elem(args, e);
   {
     const uint4* src = reinterpret_cast<const uint4*>(h.tc_mats);
     uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile_pass(C* __restrict__ amps,
     }
     fence_mbar_init();
   }
-  for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = args.coeff[e];
+  for (int e = tid; e < h.coeff_count; e += kThreads) pool[e] = pool_elem(args, e);
   __syncthreads();
 
   const long long n_tiles = h.n_tiles;

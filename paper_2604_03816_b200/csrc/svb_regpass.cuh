@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(reg_block_threads<TB, NGRP>(), (sizeof(C) == 1
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
   }
-  for (int e = tid; e < h.coeff_count; e += NTH) pool[e] = args.coeff[e];
+  for (int e = tid; e < h.coeff_count; e += NTH) pool[e] = pool_elem(args, e);
   if (h.mma_phases) {
     const uint4* src = reinterpret_cast<const uint4*>(h.tc_mats);
     uint4* dst = reinterpret_cast<uint4*>(smem + lay.mats);

@@ -18,7 +18,15 @@ constexpr int kMaxHigh = 8;        // high (strided) tile bits
 constexpr int kMaxK = 8;           // targets per kernel op
 constexpr int kMaxDenseK = 6;      // dense ops up to 64x64
 constexpr int kMaxDiagK = 8;       // merged diagonal tables up to 256 entries
-constexpr int kCoeffBytes = 24576; // coefficient pool per pass
+constexpr int kCoeffBytes = 24576; // coefficient pool per pass carried in the kernel parameters
+// Coefficient pool per pass the planner may fill (bytes): c64 passes keep the
+// parameter-block pool (k_gemm_pass shared memory is full with four 32 KB tile
+// streams and the GEMM matrices); c128 passes may grow it, the part past
+// kCoeffBytes living in global memory (PassHeader::coeff_ext) and copied into
+// shared memory with the rest at kernel start.  Diagonal tables of QFT-like
+// circuits fill it: qft-30 c128 10 -> 6 passes.
+constexpr int kPoolBytesC64 = kCoeffBytes;
+constexpr int kPoolBytesC128 = 65536;
 constexpr int kComputeWarps = 8;
 constexpr int kComputeThreads = kComputeWarps * 32;
 constexpr int kThreads = kComputeThreads + 32;   // + one TMA producer warp
@@ -102,6 +110,7 @@ struct PassHeader {
                                 // k_reg_pass tensor-core phases when mma_phases)
   int has_outside;              // some diagonal op reads shard bits outside the tile
   const float* tc_mats;         // device: tc_count * kMmaMatBytes (set at launch)
+  const void* coeff_ext;        // device: pool elements [kCoeffBytes / sizeof(C), coeff_count) (set at launch)
   int mma_phases;               // k_reg_pass: tc_mats are mma.sync B fragments
   int renorm;                   // k_reg_pass (c64 RB 5): every op is unitary -- restore
                                 // each tile's 2-norm at the end of the pass
@@ -134,5 +143,15 @@ struct PassArgs {
   OpDesc ops[kMaxOps];
   C coeff[kCoeffBytes / sizeof(C)];
 };
+
+#ifdef __CUDACC__
+// Pool element e: the parameter block holds the first kCoeffBytes, a c128
+// pass's larger pool continues in global memory.
+template <class C>
+__device__ __forceinline__ C pool_elem(const PassArgs<C>& a, int e) {
+  constexpr int kParam = kCoeffBytes / int(sizeof(C));
+  return e < kParam ? a.coeff[e] : static_cast<const C*>(a.h.coeff_ext)[e - kParam];
+}
+#endif
 
 }  // namespace svb
