@@ -542,3 +542,22 @@ def test_controls_outside_the_tile():
     finally:
         del os.environ["SVB_NO_CTRLX"]
     assert plan.num_passes <= plain.num_passes
+
+
+def test_c128_pool_past_the_parameter_block():
+    """c128 passes may hold a 64 KB coefficient pool (kPoolBytesC128): the
+    part past the 24 KB kernel-parameter block lives in global memory.  QFT
+    passes fill it with merged diagonal tables; c64 passes stay within 24 KB.
+    (The GPU QFT tests on random states run these plans against the oracle.)"""
+    param_elems = {"double": 24576 // 16, "single": 24576 // 8}
+    cap_elems = {"double": 65536 // 16, "single": 24576 // 8}
+    f16, _ = fuse(gen.qft_circuit(16), 2)
+    big = {}
+    for prec in ("double", "single"):
+        plan = CircuitPlan(16, Precision(prec), f16.gates)
+        pools = [sum(len(plan.native.kernel_op(p, i)["coeffs"])
+                     for i in range(plan.native.pass_info(p)["num_kernel_ops"]))
+                 for p in range(plan.num_passes)]
+        assert max(pools) <= cap_elems[prec]
+        big[prec] = max(pools) > param_elems[prec]
+    assert big["double"] and not big["single"]
