@@ -150,7 +150,8 @@ struct PassArgs {
 template <class C>
 __device__ __forceinline__ C pool_elem(const PassArgs<C>& a, int e) {
   constexpr int kParam = kCoeffBytes / int(sizeof(C));
-  return e < kParam ? a.coeff[e] : static_cast<const C*>(a.h.coeff_ext)[e - kParam];
+  if constexpr (kPoolBytesC64 == kCoeffBytes && sizeof(C) == 8) return a.coeff[e];  // c64: parameter block only
+  else return e < kParam ? a.coeff[e] : static_cast<const C*>(a.h.coeff_ext)[e - kParam];
 }
 #endif
 
