@@ -116,6 +116,7 @@ int device_facts(DeviceFacts** out) {
 template <class C>
 void fill_args(const Pass& p, int stages, int n_local_for_args, PassArgs<C>& a, std::vector<C>& ext) {
   std::memset(&a.h, 0, sizeof(a.h));
+  a.coeff_ext = nullptr;
   ext.clear();
   // pool elements past the parameter block go to `ext` (global memory at launch)
   constexpr int kParam = kCoeffBytes / int(sizeof(C));
@@ -551,7 +552,7 @@ void pack_tc(svb_plan* p) {
 template <class C>
 void point_ext(svb_plan* p, std::vector<PassArgs<C>>& args) {
   for (size_t i = 0; i < args.size(); ++i)
-    args[i].h.coeff_ext = p->ext_offset[i] == SIZE_MAX ? nullptr : p->ext_dev + p->ext_offset[i];
+    args[i].coeff_ext = p->ext_offset[i] == SIZE_MAX ? nullptr : reinterpret_cast<const C*>(p->ext_dev + p->ext_offset[i]);
 }
 
 int upload_ext(svb_plan* p) {

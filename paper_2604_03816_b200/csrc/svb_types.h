@@ -22,7 +22,7 @@ constexpr int kCoeffBytes = 24576; // coefficient pool per pass carried in the k
 // Coefficient pool per pass the planner may fill (bytes): c64 passes keep the
 // parameter-block pool (k_gemm_pass shared memory is full with four 32 KB tile
 // streams and the GEMM matrices); c128 passes may grow it, the part past
-// kCoeffBytes living in global memory (PassHeader::coeff_ext) and copied into
+// kCoeffBytes living in global memory (PassArgs::coeff_ext) and copied into
 // shared memory with the rest at kernel start.  Diagonal tables of QFT-like
 // circuits fill it: qft-30 c128 10 -> 6 passes.
 constexpr int kPoolBytesC64 = kCoeffBytes;
@@ -110,7 +110,6 @@ struct PassHeader {
                                 // k_reg_pass tensor-core phases when mma_phases)
   int has_outside;              // some diagonal op reads shard bits outside the tile
   const float* tc_mats;         // device: tc_count * kMmaMatBytes (set at launch)
-  const void* coeff_ext;        // device: pool elements [kCoeffBytes / sizeof(C), coeff_count) (set at launch)
   int mma_phases;               // k_reg_pass: tc_mats are mma.sync B fragments
   int renorm;                   // k_reg_pass (c64 RB 5): every op is unitary -- restore
                                 // each tile's 2-norm at the end of the pass
@@ -142,6 +141,10 @@ struct PassArgs {
   PhaseDesc phases[kMaxPhases];
   OpDesc ops[kMaxOps];
   C coeff[kCoeffBytes / sizeof(C)];
+  // device: pool elements [kCoeffBytes / sizeof(C), coeff_count) (set at
+  // launch); last, so the header, phase and op offsets of the parameter
+  // block stay as they were
+  const C* coeff_ext;
 };
 
 #ifdef __CUDACC__
@@ -151,7 +154,7 @@ template <class C>
 __device__ __forceinline__ C pool_elem(const PassArgs<C>& a, int e) {
   constexpr int kParam = kCoeffBytes / int(sizeof(C));
   if constexpr (kPoolBytesC64 == kCoeffBytes && sizeof(C) == 8) return a.coeff[e];  // c64: parameter block only
-  else return e < kParam ? a.coeff[e] : static_cast<const C*>(a.h.coeff_ext)[e - kParam];
+  else return e < kParam ? a.coeff[e] : a.coeff_ext[e - kParam];
 }
 #endif
 
