@@ -489,13 +489,27 @@ def run_b200(args):
                                 "flops_per_step": tc_flops,
                                 "note": "fp16 tcgen05 GEMM phases: 3 products (hi.hi, lo.hi, hi.lo) of a "
                                         "64x64 real block per amplitude row"},
-                     "compute": {"bound": "fp32-fma" if prec == "single" else "fp64-fma",
-                                 "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
-                                 "frac": achieved_tflops / peak_tflops,
-                                 "flops_per_amp": flops_amp,
-                                 "note": "algorithmic gate flops vs the vector FMA peak (SMs x FMA/clk x "
-                                         "2 x max SM clock); c64 GEMM phases run on the tensor cores "
-                                         "(see roofline.tensor), so this is a reference line there"}},
+                     # the pipe that executes the gate arithmetic: tcgen05 (fp16 hi/lo
+                     # products) when the plan runs GEMM phases, else the vector FMA pipe
+                     "compute": ({"bound": "tensor-fp16", "pipe": "tcgen05.mma kind::f16",
+                                  "achieved": tc_flops / (sum(pass_ms) / 1e3) / 1e12, "peak": tpeak,
+                                  "unit": "TFLOP/s", "peak_kind": tpeak_kind,
+                                  "frac": tc_flops / (sum(pass_ms) / 1e3) / 1e12 / tpeak,
+                                  "note": "GEMM-phase tensor flops (roofline.tensor); the gates' "
+                                          "algorithmic flops vs the FP32 FMA peak are in "
+                                          "compute_vector_reference"}
+                                 if tc_flops > 0 else
+                                 {"bound": "fp32-fma" if prec == "single" else "fp64-fma",
+                                  "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                                  "frac": achieved_tflops / peak_tflops, "flops_per_amp": flops_amp,
+                                  "note": "algorithmic gate flops vs the vector FMA peak (SMs x FMA/clk "
+                                          "x 2 x max SM clock)"}),
+                     "compute_vector_reference": {
+                         "bound": "fp32-fma" if prec == "single" else "fp64-fma",
+                         "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / peak_tflops, "flops_per_amp": flops_amp,
+                         "note": "algorithmic gate flops vs the vector FMA peak; above 1 when the "
+                                 "phases run on the tensor cores instead"}},
         "configs": configs,
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8 + (8 if pc == 0 else 16),
