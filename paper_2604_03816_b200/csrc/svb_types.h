@@ -24,7 +24,7 @@ constexpr int kCoeffBytes = 24576; // coefficient pool per pass carried in the k
 // streams and the GEMM matrices); c128 passes may grow it, the part past
 // kCoeffBytes living in global memory (PassArgs::coeff_ext) and copied into
 // shared memory with the rest at kernel start.  Diagonal tables of QFT-like
-// circuits fill it: qft-30 c128 10 -> 6 passes.
+// circuits fill it: qft-30 c128 10 -> 5 passes.
 constexpr int kPoolBytesC64 = kCoeffBytes;
 constexpr int kPoolBytesC128 = 65536;
 constexpr int kComputeWarps = 8;
