@@ -287,7 +287,7 @@ bool build_phases(Pass& p, int RB, int prec, int TB = 8, bool allow_ctrl = false
   // instantiated register kernels: c64 RB 3..5, c128 RB 3..4 (8 thread bits);
   // the tensor-core kernel: c64 RB 5 with 7 thread bits
   if (TB == 8 && (RB < 3 || RB > (prec == SVB_C64 ? 5 : 4))) return false;
-  // 7 thread bits: k_tc_pass / k_reg_pass<float2, 5, 7>, k_reg_pass<double2, 4, 7>
+  // 7 thread bits: k_reg_pass<float2, 5, 7> (tcgen05 phases), k_reg_pass<double2, 4, 7>
   if (TB == 7 && !((RB == 5 && prec == SVB_C64) || (RB == 4 && prec == SVB_C128))) return false;
   if (p.T != RB + TB) return false;
   for (const KernelOp& op : p.ops)

@@ -43,22 +43,6 @@ def test_registration_and_selector_tolerance():
     assert res.returncode == 0 and "ok" in res.stdout, res.stderr
 
 
-def _unused():
-    import aqsim
-    from aqsim import selector
-    import paper_2604_03816_b200 as P
-    names = {e.name for e in aqsim.registered_engines()}
-    assert {"reference", "parallel", "b200"} <= names
-    eng = aqsim.get_engine("b200")
-    assert isinstance(eng, aqsim.Engine)
-    assert eng.id.requires_accelerator
-    assert issubclass(P.AllocationError, aqsim.AllocationError)
-    if not eng.is_available():
-        choice, profiles = selector.select(aqsim.ghz_circuit(4), aqsim.registered_engines())
-        assert choice.name in {"reference", "parallel"}
-        assert all(p.engine.name != "b200" for p in profiles)
-
-
 def test_own_registry_has_b200():
     import paper_2604_03816_b200 as P
     assert "b200" in {e.name for e in P.registered_engines()}

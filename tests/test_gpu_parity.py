@@ -306,9 +306,9 @@ def test_layered33_c128_mirror_full_size(eng):
 
 
 def test_reference_registry_dropin():
-    """With the reference package importable, ``aqsim.run_circuit("b200")`` runs
-    on the device and matches the reference engine (skipped on the GPU box,
-    where /root/reference is absent)."""
+    """With the reference package importable (baseline/_ref travels to the GPU
+    box; tests/conftest.py appends it), ``aqsim.run_circuit("b200")`` runs on
+    the device and matches the reference engine."""
     aqsim = pytest.importorskip("aqsim")
     import paper_2604_03816_b200  # noqa: F401  (registers "b200")
     c = aqsim.qft_circuit(8)
@@ -316,6 +316,21 @@ def test_reference_registry_dropin():
     want = aqsim.run_circuit("reference", c, aqsim.Precision.DOUBLE)
     assert np.abs(got.amplitudes - want.amplitudes).max() <= 1e-12
     assert aqsim.state_fidelity(got, want) == pytest.approx(1.0, abs=1e-10)
+
+
+def test_reference_selector_profiles_the_device_engine():
+    """aqsim's own selector (ref selector.py:93-118, 127-170) benchmarks every
+    available engine through the plugin API -- init_state / apply_gate /
+    synchronize / release -- and here that includes the device engine."""
+    aqsim = pytest.importorskip("aqsim")
+    from aqsim import selector
+    import paper_2604_03816_b200  # noqa: F401  (registers "b200")
+    engines = aqsim.registered_engines()
+    assert "b200" in {e.name for e in engines}
+    choice, profiles = selector.select(aqsim.ghz_circuit(16), engines)
+    prof = {p.engine.name: p for p in profiles}
+    assert "b200" in prof and prof["b200"].throughput > 0
+    assert choice.name in prof
 
 
 def test_cli_run_and_bench_scaling(capsys):
